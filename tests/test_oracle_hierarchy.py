@@ -1,0 +1,158 @@
+"""Pins for the oracle hierarchy, prolongation and driver."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+import oracle
+from tests import helpers as H
+from workloads import configs, graphs
+
+
+def _check_level_pair(fine: oracle.Level, coarse: oracle.Level):
+    P = fine.parent
+    n, k = fine.n, coarse.n
+    # parent surjective, clusters of size 1 or 2 (a matching)
+    sizes = np.bincount(P, minlength=k)
+    assert sizes.min() >= 1 and sizes.max() <= 2 and sizes.shape[0] == k
+    # node weights conserved per cluster
+    np.testing.assert_array_equal(np.bincount(P, weights=fine.c, minlength=k).astype(np.int64), coarse.c)
+    # coarse omega = brute-force crossing sums  Pm^T A Pm  off the diagonal
+    A = sp.csr_matrix((fine.omega.astype(np.float64), fine.col, fine.row_ptr), shape=(n, n))
+    Pm = sp.csr_matrix((np.ones(n), (np.arange(n), P)), shape=(n, k))
+    C = (Pm.T @ A @ Pm).tocsr()
+    C.setdiag(0)
+    C.eliminate_zeros()
+    C.sort_indices()
+    np.testing.assert_array_equal(C.indptr, coarse.row_ptr)
+    np.testing.assert_array_equal(C.indices, coarse.col)
+    np.testing.assert_array_equal(C.data.astype(np.int64), coarse.omega)
+    # every matched pair is an edge of the fine graph
+    rows = np.repeat(np.arange(n), np.diff(fine.row_ptr))
+    edges = set(zip(rows.tolist(), fine.col.tolist()))
+    for cl in np.nonzero(sizes == 2)[0][:2000]:
+        a, b = np.nonzero(P == cl)[0]
+        assert (a, b) in edges
+    # coarse ids are ranks of leaders min(u, mate(u)) in ascending order
+    leaders = np.array([np.nonzero(P == c)[0].min() for c in range(min(k, 500))])
+    assert np.all(np.diff(leaders) > 0)
+
+
+def _maximal(fine: oracle.Level) -> bool:
+    P = fine.parent
+    sizes = np.bincount(P)
+    single = sizes[P] == 1
+    rows = np.repeat(np.arange(fine.n), np.diff(fine.row_ptr))
+    return not np.any(single[rows] & single[fine.col])
+
+
+@pytest.mark.parametrize("name", ["cfg3_mesh64", "cfg5_grid16", "cfg1"])
+def test_p11_hierarchy_invariants(name):
+    w = configs.make(name)
+    lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=100)
+    assert len(lv) >= 2
+    for l in range(len(lv) - 1):
+        _check_level_pair(lv[l], lv[l + 1])
+        assert lv[l + 1].n <= 0.9 * lv[l].n
+        if lv[l].rounds < 64:
+            assert _maximal(lv[l])
+    assert lv[-1].n <= 100 or lv[-1].parent is None
+    assert lv[0].c.sum() == lv[-1].c.sum() == w.n
+
+
+def test_p11_hierarchy_chung_lu_small():
+    w = configs.make("cfg4_cl20000")
+    lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=1000)
+    for l in range(len(lv) - 1):
+        _check_level_pair(lv[l], lv[l + 1])
+    assert lv[-1].n <= 1000
+
+
+def test_p11_triangle_hand_instance():
+    """Triangle a,b,c with omega(a,b)=1, (a,c)=2, (b,c)=3, unit c: every vertex's
+    best is its heaviest edge; b and c pick each other, a stays single.
+    Coarse: {a} (id 0, c=1), {b,c} (id 1, c=2), one edge with omega 1+2 = 3
+    (the crossing edges)."""
+    g = graphs.from_edges(3, np.array([0, 0, 1]), np.array([1, 2, 2]))
+    # CSR rows: 0:[1,2] 1:[0,2] 2:[0,1]
+    om = np.array([1, 2, 1, 3, 2, 3], dtype=np.int64)
+    lv = oracle.build_hierarchy(g, seed=1, n_stop=1, omega=om)
+    assert lv[0].parent.tolist() == [0, 1, 1]
+    assert lv[1].c.tolist() == [1, 2]
+    assert lv[1].col.tolist() == [1, 0] and lv[1].omega.tolist() == [3, 3]
+
+
+def test_p11_rating_normalised_by_weights():
+    """Rating omega / (c_u c_v): with omega equal, the lighter neighbour wins."""
+    # star: centre 0, leaves 1 (c=5), 2 (c=1), 3 (c=3); unit omega
+    g = graphs.from_edges(4, np.array([0, 0, 0]), np.array([1, 2, 3]))
+    c = np.array([1, 5, 1, 3], dtype=np.int64)
+    lv = oracle.build_hierarchy(g, seed=9, n_stop=1, c=c)
+    P = lv[0].parent
+    assert P[0] == P[2] and P[1] != P[0] and P[3] != P[0]
+
+
+def test_hierarchy_deterministic_and_seed_dependent():
+    w = configs.make("cfg3_mesh64")
+    a = oracle.build_hierarchy(w.graph, seed=5)
+    b = oracle.build_hierarchy(w.graph, seed=5)
+    c = oracle.build_hierarchy(w.graph, seed=6)
+    assert all(np.array_equal(x.parent, y.parent) for x, y in zip(a[:-1], b[:-1]))
+    assert not np.array_equal(a[0].parent, c[0].parent)
+
+
+def test_p13_prolongation_bounds_and_rng():
+    rng = np.random.default_rng(3)
+    parent = rng.integers(0, 50, 400).astype(np.int32)
+    xc = rng.normal(size=(50, 3))
+    x = oracle.prolong(parent, xc, seed=77, level=2)
+    dev = x - xc[parent]
+    assert np.all(np.abs(dev) <= 1e-3)
+    # the jitter is 1e-3 (2U - 1) with U the counter RNG of (seed, JITTER, level, u*dim + k)
+    u, k = 123, 2
+    U = oracle.uniform24(oracle.key_vertex(77, oracle.TAG_JITTER, 2, u, 3, k))
+    assert dev[u, k] == pytest.approx(1e-3 * (2 * U - 1), abs=1e-15)
+    # different levels -> different draws
+    x2 = oracle.prolong(parent, xc, seed=77, level=3)
+    assert not np.array_equal(x, x2)
+
+
+def test_init_box_range():
+    x = oracle.init_box(500, 2, 7.5, seed=4, level=6)
+    assert x.min() >= 0.0 and x.max() < 7.5
+    U = oracle.uniform24(oracle.key_vertex(4, oracle.TAG_INIT, 6, 17, 2, 1))
+    assert x[17, 1] == 7.5 * U
+
+
+def test_coarse_sset_distances():
+    """P:247-248 / Q7: d = c_u^(1/dim) + c_v^(1/dim), w = d^-2."""
+    lvl = oracle.Level(n=2, row_ptr=np.array([0, 1, 2]), col=np.array([1, 0], dtype=np.int32),
+                       omega=np.array([1, 1]), c=np.array([4, 9]), parent=None, rounds=0)
+    cs = oracle.coarse_sset(lvl, 2)
+    np.testing.assert_allclose(cs.d, [5.0, 5.0])
+    np.testing.assert_allclose(cs.w, [0.04, 0.04])
+    lvl3 = oracle.Level(n=2, row_ptr=np.array([0, 1, 2]), col=np.array([1, 0], dtype=np.int32),
+                        omega=np.array([1, 1]), c=np.array([8, 27]), parent=None, rounds=0)
+    np.testing.assert_allclose(oracle.coarse_sset(lvl3, 3).d, [5.0, 5.0], rtol=1e-15)
+
+
+def test_layout_h0_equals_repeated_sweeps():
+    w = configs.make("cfg1_grid12")
+    x0 = w.x0.astype(np.float64)
+    x, e, nl = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [5], w.seed, x_init=x0)
+    y = x0
+    for _ in range(5):
+        y = oracle.sweep_exact(w.S, y, w.alpha, w.q)
+    np.testing.assert_array_equal(x, y)
+    np.testing.assert_allclose(e, oracle.energy(w.S, y, w.alpha, w.q), rtol=0)
+    assert nl == 1
+
+
+def test_layout_multilevel_small_runs():
+    w = configs.make("cfg3_mesh32")
+    x, e, nl = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 2, [4], w.seed, n_stop=100)
+    assert nl >= 3 and np.all(np.isfinite(x)) and np.isfinite(e[2])
+    # the finest-level result is a pure function of the seed
+    x2, e2, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 2, [4], w.seed, n_stop=100)
+    np.testing.assert_array_equal(x, x2)
