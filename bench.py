@@ -1,0 +1,360 @@
+#!/usr/bin/env python3
+"""MulMent hot-path benchmark (driver contract).
+
+A STEP is one pass of the whole hot path over one batch of synthetic input:
+one mm_layout call on BASELINE.json configs[1] (RGG, n = 65,428 after LCC,
+S = hop <= 2 pairs, q = 0, alpha = 0.01, 20 exact Jacobi sweeps + the final
+Eq.(1) energy).  `value` = vertex-updates/s (n x sweeps per step, summed over
+ranks) with inputs resident in HBM; `e2e` = the same metric through the public
+API with the inputs copied from pinned host memory and the layout + energy
+copied back inside the timed region.
+
+Multi-GPU: the north star is one GPU with no sharding, so --gpus N runs N
+independent replicas ("replicas only"); value = units of all
+ranks / max-over-ranks time.
+
+--impl reference: this build has no installable reference implementation; the
+reference arm is the FP64 oracle (oracle/), timed as it stands on the host
+cores on a bounded row sample of the same sweep.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "vertex-updates/s per sweep and repulsion pair-interactions/s; % of FP32/HBM roofline"
+UNIT = "vertex-updates/s"
+SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
+FP32_PEAK_TFLOPS = SM_COUNT * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12  # 74.4, derived
+MUFU_PER_CLK_SM = 16
+FLOP_PER_PAIR = 10  # 2D q = 0 pair: 2 sub + 2 fma (r^2) + 2 fma (acc), FMA = 2
+
+
+# ------------------------------------------------------------------ distributed plumbing
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(value: float, device=None) -> float:
+    """All-reduce MAX of a scalar (NCCL on GPU, gloo on CPU); identity for 1 rank."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(value: float, device=None) -> float:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return value
+    t = torch.tensor([value], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def barrier():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [t.strip() for t in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                smax.append(float(p[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(smax), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ workload
+def load_workload(name: str):
+    from workloads import configs
+
+    return configs.make(name)
+
+
+def cpu_oracle_sample(w, target_s: float = 8.0, max_rows=None):
+    """Time the oracle as it stands (FP64, all host cores via OpenMP) on a
+    bounded row sample of one exact sweep of the workload."""
+    import numpy as np
+
+    import oracle
+
+    cores = oracle.default_threads()
+    x = w.x0.astype(np.float64)
+    rng = np.random.default_rng(0)
+    calib = np.sort(rng.choice(w.n, size=min(w.n, 256 * cores), replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.sweep_exact(w.S, x, w.alpha, w.q, rows=calib, nthreads=cores)
+    dt = time.perf_counter() - t0
+    rate = calib.shape[0] / max(dt, 1e-9)
+    rows_n = int(min(w.n, max_rows or w.n, max(calib.shape[0], rate * target_s)))
+    rows = np.sort(rng.choice(w.n, size=rows_n, replace=False)).astype(np.int32)
+    return rows, cores
+
+
+def run_reference(args):
+    """--impl reference: the FP64 oracle on the host cores (rank 0 only)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+
+    w = load_workload(args.config)
+    rows, cores = cpu_oracle_sample(w, target_s=args.ref_step_s)
+    x = w.x0.astype(np.float64)
+    for _ in range(args.warmup):
+        oracle.sweep_exact(w.S, x, w.alpha, w.q, rows=rows[: max(1, rows.shape[0] // 8)], nthreads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.sweep_exact(w.S, x, w.alpha, w.q, rows=rows, nthreads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = rows.shape[0] * args.steps / tot
+    sample = (f"{rows.shape[0]} of {w.n} rows of one exact Eq.(2) sweep of {args.config} per step "
+              f"(each row: |S_i| gathers + {w.n - 1} pair terms, FP64)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(w, args),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "pair_interactions_per_s": value * (w.n - 1)}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_block(w, args):
+    return {"workload": f"{w.name}: BASELINE.json configs[1] (RGG n=65,536 -> LCC n={w.n}, S = hop<=2, "
+                        f"|S|={w.S.nnz}, q={w.q}, alpha={w.alpha}, dim={w.dim}, {w.sweeps} exact sweeps + energy)",
+            "n": w.n, "nnz_S": w.S.nnz, "sweeps_per_step": w.sweeps, "dim": w.dim, "q": w.q, "alpha": w.alpha,
+            "l2": "flushed (256 MB write) between timed steps; per-step CUDA events",
+            "parallelism": f"replicas x{args.gpus}"}
+
+
+# ------------------------------------------------------------------ GPU arm
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1506_04383_b200 as mm
+
+    ws, rank, local = dist_env()
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    mm.load()
+    w = load_workload(args.config)
+    n, K = w.n, w.sweeps
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    with torch.cuda.stream(stream):
+        S = mm.sset_to_device(w.S, dev)
+        x0 = mm.coords_to_device(w.x0, dev)
+        out = torch.empty_like(x0)
+
+        def step():
+            return mm.layout(None, S, w.dim, w.alpha, w.q, 0, [K], w.seed, x_init=x0, out=out)
+
+        for _ in range(args.warmup):
+            _, rep = step()
+        torch.cuda.synchronize(dev)
+
+        # ---- timed region (device-resident inputs)
+        clocks = ClockSampler(local)
+        clocks.start()
+        mm.profile_reset()
+        mm.profile_enable(True)
+        l0 = mm.launch_count()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        torch.cuda.synchronize(dev)
+        for s in range(args.steps):
+            flush.fill_(float(s))  # evict L2 between timed steps (outside the event pair)
+            ev[s][0].record(stream)
+            _, rep = step()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        launches = mm.launch_count() - l0
+        prof = mm.profile_read()
+        mm.profile_enable(False)
+        clk = clocks.stop()
+        dev_ms = sum(a.elapsed_time(b) for a, b in ev)
+        ms_step = max_over_ranks(dev_ms / args.steps, dev)
+
+        # ---- e2e through the public API with host buffers
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        h_rp, h_col = pin(w.S.row_ptr.astype(np.int64)), pin(w.S.col.astype(np.int32))
+        h_d, h_w = pin(w.S.d.astype(np.float32)), pin(w.S.w.astype(np.float32))
+        h_x = pin(mm.coords_layout(w.x0))
+        h_out = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
+        d_rp, d_col = torch.empty_like(h_rp, device=dev), torch.empty_like(h_col, device=dev)
+        d_d, d_w, d_x = torch.empty_like(h_d, device=dev), torch.empty_like(h_w, device=dev), torch.empty_like(h_x, device=dev)
+        Se = mm.DeviceSSet(d_rp, d_col, d_d, d_w)
+        h2d = sum(t.numel() * t.element_size() for t in (h_rp, h_col, h_d, h_w, h_x))
+        d2h = h_out.numel() * h_out.element_size() + 3 * 8  # layout + (stress, entropy, energy)
+
+        def e2e_step():
+            for hd, dd in ((h_rp, d_rp), (h_col, d_col), (h_d, d_d), (h_w, d_w), (h_x, d_x)):
+                dd.copy_(hd, non_blocking=True)
+            y, r = mm.layout(None, Se, w.dim, w.alpha, w.q, 0, [K], w.seed, x_init=d_x, out=out)
+            h_out.copy_(y, non_blocking=True)
+            return r
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for s in range(args.steps):
+            flush.fill_(float(s))
+            ev2[s][0].record(stream)
+            e2e_step()
+            ev2[s][1].record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev2) / args.steps, dev)
+
+    units = sum_over_ranks(float(n * K), dev)
+    value = units / (ms_step / 1e3)
+    pairs_step = n * (n - 1) * K
+    kern = prof.get("repulse_exact", {"launches": 0, "total_ms": float("nan")})
+    k_ms = kern["total_ms"] / max(kern["launches"], 1)
+    achieved_tflops = FLOP_PER_PAIR * n * (n - 1) / (k_ms / 1e3) / 1e12
+    step_share = {k: v["total_ms"] / max(dev_ms, 1e-9) for k, v in prof.items()}
+    if rank != 0:
+        return 0
+    cpu = None
+    if ws == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        rows, cores = cpu_oracle_sample(w, target_s=args.cpu_s)
+        t0 = time.perf_counter()
+        oracle.sweep_exact(w.S, w.x0.astype(np.float64), w.alpha, w.q, rows=rows, nthreads=cores)
+        dt = time.perf_counter() - t0
+        cpu = {"value": rows.shape[0] / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{rows.shape[0]} of {n} rows of one exact Eq.(2) sweep of {w.name} "
+                         f"(FP64, OpenMP over rows), {dt:.1f} s"}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": config_block(w, args),
+        "pair_interactions_per_s": ws * pairs_step / (ms_step / 1e3),
+        "roofline": {"bound": "alu", "kernel": "repulse_exact (b)", "achieved": achieved_tflops,
+                     "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_TFLOPS,
+                     "traffic": None,
+                     "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (DESIGN.md §5)",
+                     "flop_per_pair": FLOP_PER_PAIR, "pairs_per_launch": n * (n - 1),
+                     "avg_launch_ms": k_ms,
+                     "mufu_ceiling_frac": MUFU_PER_CLK_SM * FLOP_PER_PAIR / (2.0 * FP32_LANES),
+                     "pairs_per_s_kernel": n * (n - 1) / (k_ms / 1e3)},
+        "kernel_share_of_step": step_share,
+        "kernels": prof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": units / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+        "gpu_launches": launches,
+        "clocks": clk,
+        "energy_last_step": rep["energy"],
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="mm", choices=["mm", "reference"])
+    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--cpu-s", type=float, default=10.0)
+    ap.add_argument("--ref-step-s", type=float, default=6.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "mm":
+        print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,222 @@
+/* mm.h — C-ABI of the B200-native MulMent hot path (libmm_b200.so).
+ *
+ * Meyerhenke, Nöllenburg, Schulz, "Drawing large graphs by multilevel
+ * maxent-stress optimization", arXiv 1506.04383.  Citations "P:n" are lines of
+ * the paper's LaTeX source; "Qn" are the readings of DESIGN.md §3.
+ *
+ * What the library computes (one GPU, hand-written sm_100a CUDA kernels):
+ *   - mm_sweep: one synchronous (Jacobi) sweep of the local update Eq.(2)
+ *     (P:176-181), or of Eq.(3) when a coarse-level map is given;
+ *   - mm_energy: the maxent-stress energy Eq.(1);
+ *   - mm_build_hierarchy: the matching-based multilevel hierarchy with the
+ *     contraction of P:225-232 (matching per Q16, stop rule Q17);
+ *   - mm_layout: the multilevel driver (P:195-257 with fixed alpha).
+ *
+ * Conventions (all entry points):
+ *   - POINTERS are DEVICE pointers unless the comment says "host".  The caller
+ *     owns every input and output buffer; the library owns only what it
+ *     returns through an opaque handle (mm_hierarchy) and its internal scratch.
+ *   - COORDINATES: dim 2 -> float[2n] interleaved (x0,y0,x1,y1,...), 8-byte
+ *     aligned; dim 3 -> float[4n] (x,y,z,pad per vertex), 16-byte aligned; the
+ *     pad lane is ignored on input and written 0 on output.
+ *   - CSR: row_ptr int64[n+1] (row_ptr[0] = 0), col int32[nnz]; rows need not
+ *     be sorted; S rows must not contain i itself or duplicates.
+ *   - STREAMS: every call enqueues on `stream` (a cudaStream_t; NULL = legacy
+ *     default stream).  Calls marked "async" do not synchronise the host;
+ *     calls marked "syncs" synchronise `stream` before returning.
+ *   - ERRORS: argument checks are synchronous and happen before any launch;
+ *     on error nothing is enqueued and mm_last_error() holds a thread-local
+ *     message.  Device-detected problems (non-finite coordinates) are written
+ *     to mm_sweep_stats.flags and reported as MM_ERR_NONFINITE by the next
+ *     syncing call that reads them.  No C++ exception crosses this ABI.
+ *   - There is no CPU fallback: a missing or unusable GPU is MM_ERR_CUDA.
+ */
+#ifndef MM_H
+#define MM_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MM_API __attribute__((visibility("default")))
+#else
+#define MM_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* mm_stream_t; /* a cudaStream_t */
+
+typedef enum {
+    MM_OK = 0,
+    MM_ERR_INVALID_ARGUMENT = -1, /* null pointer, bad size, aliasing, bad dim */
+    MM_ERR_INVALID_INPUT = -2,    /* bad CSR / rho_i <= 0 detected by validation */
+    MM_ERR_NONFINITE = -3,        /* non-finite coordinate produced or given; coincident non-S pair in mm_energy */
+    MM_ERR_OUT_OF_MEMORY = -4,
+    MM_ERR_CUDA = -5,             /* a CUDA runtime error (no device, launch failure, ...) */
+    MM_ERR_UNSUPPORTED = -6       /* dim not 2|3, q < 0 */
+} mm_status;
+
+/* Graph G = (V, E, c, omega), symmetric CSR of E. */
+typedef struct {
+    int32_t n;
+    int64_t nnz;              /* = 2|E| */
+    const int64_t* row_ptr;   /* device int64[n+1] */
+    const int32_t* col;       /* device int32[nnz] */
+    const int32_t* omega;     /* device int32[nnz] edge weights, or NULL = unit */
+} mm_graph;
+
+/* Stress pair set S ⊇ E (P:163 footnote): per-vertex rows S_i with target
+ * distance d_ij > 0 and weight w_ij >= 0 (w = d^-2 by default).
+ * Row i must have rho_i = sum_j w_ij > 0. */
+typedef struct {
+    int32_t n;
+    int64_t nnz;
+    const int64_t* row_ptr;   /* device int64[n+1] */
+    const int32_t* col;       /* device int32[nnz] */
+    const float* d;           /* device float[nnz] */
+    const float* w;           /* device float[nnz] */
+} mm_sset;
+
+/* Coarse-level map for Eq.(3): parent P (one level up, defines
+ * the same-cluster sum) and ancestor H (level l+h', defines the coarse
+ * representatives, k of them; H must be surjective onto 0..k-1). */
+typedef struct {
+    int32_t k;
+    const int32_t* parent;    /* device int32[n] */
+    const int32_t* ancestor;  /* device int32[n], values in [0,k) */
+} mm_approx;
+
+/* Device-side per-sweep statistics (written by mm_sweep when non-NULL). */
+typedef struct {
+    double dx2;       /* sum_i |x'_i - x_i|^2 */
+    double x2;        /* sum_i |x_i|^2 ; relative change = sqrt(dx2 / x2) */
+    double stress;    /* 1/2 sum_i sum_{j in S_i} w (|x_i - x_j| - d)^2 at the INPUT x */
+    int32_t flags;    /* bit 0: non-finite output coordinate */
+    int32_t pad;
+} mm_sweep_stats;
+
+typedef struct mm_hierarchy mm_hierarchy;
+
+/* Host view of one hierarchy level; array members are device pointers owned
+ * by the hierarchy and valid until mm_hierarchy_free. */
+typedef struct {
+    int32_t n;
+    int64_t nnz;
+    const int64_t* row_ptr;
+    const int32_t* col;
+    const int32_t* omega;   /* coarse edge weights (sum of crossing weights) */
+    const int32_t* c;       /* node weights (sum of member weights) */
+    const int32_t* parent;  /* int32[n] -> level l+1 ids; NULL at the coarsest level */
+    const float* d;         /* coarse S^l = E^l distances (Q7); NULL at level 0 */
+    const float* w;         /* coarse weights d^-2; NULL at level 0 */
+    int32_t rounds;         /* matching rounds used to build level l+1 */
+} mm_level_view;
+
+/* Layout report (host). */
+#define MM_MAX_LEVELS 64
+typedef struct {
+    int32_t levels;
+    int32_t n_level[MM_MAX_LEVELS];
+    int32_t k_level[MM_MAX_LEVELS];     /* approximation-level size used at level l (0 = exact) */
+    double stress, entropy, energy;     /* mm_energy of the final finest layout (Eq.(1)) */
+    double rel_change;                  /* relative change of the last finest-level sweep */
+    int64_t vertex_updates;             /* sum_l n_l * K_l */
+    int64_t pair_interactions;          /* repulsion pairs evaluated (DESIGN.md §5 convention) */
+} mm_layout_report;
+
+/* ------------------------------------------------------------------ API */
+
+/* Human-readable status / thread-local detail of the last error. */
+MM_API const char* mm_status_string(mm_status s);
+MM_API const char* mm_last_error(void);
+/* Library version string, e.g. "mm_b200 0.1 sm_100a". */
+MM_API const char* mm_version(void);
+
+/* Optional allocator hook for the library's scratch and hierarchy storage.
+ * alloc(bytes, stream, ctx) must return device memory usable on `stream`;
+ * free_(ptr, stream, ctx) releases it.  NULL, NULL restores the default
+ * (cudaMallocAsync / cudaFreeAsync, stream-ordered). */
+MM_API mm_status mm_set_allocator(void* (*alloc)(size_t, mm_stream_t, void*),
+                           void (*free_)(void*, mm_stream_t, void*), void* ctx);
+
+/* Scratch bytes mm_sweep needs for n vertices (host out). ap = NULL: exact. */
+MM_API mm_status mm_sweep_workspace(int32_t n, int dim, const mm_approx* ap, size_t* bytes);
+
+/* One Jacobi sweep, Eq.(2) (ap = NULL: exact entropy term over all j notin S_i,
+ * P:178) or Eq.(3) (ap != NULL: same-cluster exact terms over P, nu-weighted
+ * representatives over H excluding H(i), minus the S_i terms).
+ * q >= 0 is the repulsion exponent: r(i,j) = (x_i - x_j)/|x_i - x_j|^(q+2)
+ * (q = 0 is the paper's r-value).  The representatives are the
+ * unweighted means of x_in over each H class (Q11/Q12).
+ * x_out must not alias x_in.  ws/ws_bytes: caller scratch of at least
+ * mm_sweep_workspace() bytes, or NULL/0 to let the library allocate it
+ * stream-ordered.  stats (device, nullable) receives mm_sweep_stats.  async. */
+MM_API mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap,
+                   const float* x_in, float* x_out, mm_sweep_stats* stats,
+                   void* ws, size_t ws_bytes, mm_stream_t stream);
+
+/* Maxent-stress energy Eq.(1) in the S form with readings Q3/Q4:
+ * out[0] = stress = 1/2 sum_i sum_{j in S_i} w (|x_i-x_j| - d)^2
+ * out[1] = entropy = 1/2 sum_i sum_{j notin S_i, j != i} phi_q(|x_i - x_j|),
+ *          phi_0(r) = -ln r, phi_q(r) = r^-q / q
+ * out[2] = stress + alpha * entropy.  out is HOST double[3].
+ * FP32 per pair, FP64 accumulation, fixed summation order (deterministic).
+ * A coincident non-S pair returns MM_ERR_NONFINITE.  syncs. */
+MM_API mm_status mm_energy(const mm_sset* S, int dim, double alpha, double q, const float* x,
+                    double* out, mm_stream_t stream);
+
+/* Build the hierarchy: handshake heavy-edge matching by rating
+ * omega_uv / (c_u c_v) (exact int64 compare; ties: higher SplitMix64 hash of
+ * (seed, level, round, min, max), then lower id; <= max_rounds rounds), leader
+ * ranking, contraction, coarse S^l (Q7, needs dim), until
+ * n_l <= n_stop or a contraction would keep > 90% of the vertices or
+ * max_levels levels exist (Q17).  c: device int32[n] node weights or NULL =
+ * unit.  Integer results are bit-identical to the oracle's.  Syncs once per
+ * level (to read n_{l+1}).  *out is released with mm_hierarchy_free. */
+MM_API mm_status mm_build_hierarchy(const mm_graph* g, const int32_t* c, int dim, uint64_t seed,
+                             int32_t n_stop, int32_t max_levels, int32_t max_rounds,
+                             mm_hierarchy** out, mm_stream_t stream);
+MM_API int32_t mm_hierarchy_num_levels(const mm_hierarchy* h);
+MM_API mm_status mm_hierarchy_level(const mm_hierarchy* h, int32_t level, mm_level_view* out /*host*/);
+MM_API void mm_hierarchy_free(mm_hierarchy* h);
+/* Copy level `level` of the hierarchy into HOST arrays (any may be NULL to
+ * skip): row_ptr int64[n+1], col int32[nnz], omega int32[nnz], c int32[n],
+ * parent int32[n] (not at the coarsest level), d/w float[nnz] (not at level 0).
+ * syncs `stream`. */
+MM_API mm_status mm_hierarchy_copy_level(const mm_hierarchy* h, int32_t level, int64_t* row_ptr, int32_t* col,
+                                         int32_t* omega, int32_t* c, int32_t* parent, float* d, float* w,
+                                         mm_stream_t stream);
+
+/* Multilevel layout.  h = 0: single level, x_init (device, required) is
+ * iterated sweeps[0] exact sweeps (Eq.(2)).  h > 0: hierarchy (n_stop, seed),
+ * box init of the coarsest level L (Q14), sweeps[min(L, nsweeps-1)] exact
+ * sweeps there, then for l = L-1..0: prolongation (Q15) and
+ * sweeps[min(l, nsweeps-1)] Eq.(3) sweeps with h' = min(h, L-l) (Q13); coarse
+ * levels use S^l (Q7), level 0 uses S.  sweeps: HOST int32[nsweeps].
+ * x_out: device, the finest layout.  rep: HOST report (nullable).  syncs. */
+MM_API mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, float alpha, float q, int h,
+                    const int32_t* sweeps, int32_t nsweeps, uint64_t seed, int32_t n_stop,
+                    const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream);
+
+/* ------------------------------------------------------------------ instrumentation */
+/* Total kernels launched by this library since load (host counter). */
+MM_API int64_t mm_launch_count(void);
+/* When enabled, every kernel launch is bracketed by CUDA events on its
+ * stream; mm_profile_read syncs those events and returns, per kernel name,
+ * the launch count and summed device milliseconds. */
+typedef struct {
+    char name[48];
+    int64_t launches;
+    double total_ms;
+} mm_kernel_profile;
+MM_API mm_status mm_profile_enable(int on);
+MM_API mm_status mm_profile_reset(void);
+/* writes up to max entries into out (host); *count = number of kernel names */
+MM_API mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MM_H */

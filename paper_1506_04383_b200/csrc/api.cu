@@ -1,0 +1,971 @@
+// api.cu — the C-ABI of libmm_b200.so (include/mm.h): argument checks, the
+// stream-ordered allocator hook, workspace layout, launch bookkeeping and the
+// host drivers (mm_sweep, mm_energy, mm_build_hierarchy, mm_layout).
+// Every step of the hot path runs in the kernels of k_repulse.cu, k_gather.cu
+// and k_hier.cu; the host only sequences launches and reads sizes.
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <atomic>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "k_hier.cuh"
+#include "k_repulse.cuh"
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string g_err;
+
+void set_err(const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+}
+
+mm_status cuda_fail(cudaError_t e, const char* where) {
+    set_err("%s: %s", where, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? MM_ERR_OUT_OF_MEMORY : MM_ERR_CUDA;
+}
+
+#define MM_CU(expr, where)                              \
+    do {                                                \
+        cudaError_t _e = (expr);                        \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+// ------------------------------------------------------------------ allocator
+void* (*g_alloc)(size_t, mm_stream_t, void*) = nullptr;
+void (*g_free)(void*, mm_stream_t, void*) = nullptr;
+void* g_alloc_ctx = nullptr;
+
+void* dev_alloc(size_t bytes, cudaStream_t st) {
+    if (bytes == 0) bytes = 16;
+    if (g_alloc) return g_alloc(bytes, (mm_stream_t)st, g_alloc_ctx);
+    void* p = nullptr;
+    if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return p;
+}
+void dev_free(void* p, cudaStream_t st) {
+    if (!p) return;
+    if (g_free) g_free(p, (mm_stream_t)st, g_alloc_ctx);
+    else cudaFreeAsync(p, st);
+}
+
+// A bump allocator over one device block (workspace carving, 256-B aligned).
+struct Carver {
+    char* base;
+    size_t cap, off = 0;
+    bool ok = true;
+    Carver(void* b, size_t c) : base((char*)b), cap(c) {}
+    template <class T>
+    T* take(size_t count) {
+        size_t bytes = ((count * sizeof(T)) + 255) & ~(size_t)255;
+        if (off + bytes > cap) {
+            ok = false;
+            return nullptr;
+        }
+        T* p = reinterpret_cast<T*>(base + off);
+        off += bytes;
+        return p;
+    }
+};
+size_t al(size_t bytes) { return (bytes + 255) & ~(size_t)255; }
+
+struct DevBuf {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    DevBuf() = default;
+    DevBuf(size_t bytes, cudaStream_t s) : st(s) { p = dev_alloc(bytes, s); }
+    ~DevBuf() { dev_free(p, st); }
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// ------------------------------------------------------------------ profiling
+std::atomic<int64_t> g_launches{0};
+std::atomic<int> g_prof_on{0};
+std::mutex g_prof_mu;
+struct PendingEv {
+    const char* name;
+    cudaEvent_t a, b;
+};
+std::vector<PendingEv> g_pending;
+std::map<std::string, std::pair<int64_t, double>> g_prof;
+
+}  // namespace
+
+namespace mm {
+LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), stream(s), slot(-1) {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    if (!g_prof_on.load(std::memory_order_relaxed)) return;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
+    PendingEv ev{n, nullptr, nullptr};
+    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) return;
+    cudaEventRecord(ev.a, s);
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    g_pending.push_back(ev);
+    slot = (int)g_pending.size() - 1;
+}
+LaunchScope::~LaunchScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    if (slot < (int)g_pending.size()) cudaEventRecord(g_pending[slot].b, stream);
+}
+}  // namespace mm
+
+using namespace mm;
+
+// ------------------------------------------------------------------ helpers
+namespace {
+
+int stride_of(int dim) { return dim == 2 ? 2 : 4; }
+
+mm_status check_sset(const mm_sset* S, const char* who) {
+    if (!S) { set_err("%s: S is NULL", who); return MM_ERR_INVALID_ARGUMENT; }
+    if (S->n <= 0) { set_err("%s: S->n must be > 0 (got %d)", who, S->n); return MM_ERR_INVALID_ARGUMENT; }
+    if (S->nnz < 0) { set_err("%s: S->nnz < 0", who); return MM_ERR_INVALID_ARGUMENT; }
+    if (!S->row_ptr || (S->nnz > 0 && (!S->col || !S->d || !S->w))) {
+        set_err("%s: S has a NULL array", who);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    return MM_OK;
+}
+
+mm_status check_dim_q(int dim, double q, const char* who) {
+    if (dim != 2 && dim != 3) { set_err("%s: dim must be 2 or 3 (got %d)", who, dim); return MM_ERR_UNSUPPORTED; }
+    if (!(q >= 0.0) || !isfinite(q)) { set_err("%s: q must be finite and >= 0", who); return MM_ERR_UNSUPPORTED; }
+    return MM_OK;
+}
+
+mm_status check_x(const float* x, int dim, const char* what, const char* who) {
+    if (!x) { set_err("%s: %s is NULL", who, what); return MM_ERR_INVALID_ARGUMENT; }
+    const uintptr_t a = dim == 2 ? 8 : 16;
+    if (((uintptr_t)x) % a) { set_err("%s: %s must be %d-byte aligned", who, what, (int)a); return MM_ERR_INVALID_ARGUMENT; }
+    return MM_OK;
+}
+
+// Buffers for one sweep (all device); sized by plan_sweep_bytes.
+struct SweepBufs {
+    float* part = nullptr;
+    double* stat_partial = nullptr;
+    int32_t* flags = nullptr;
+    float4* reps = nullptr;
+    int32_t* mptr = nullptr;
+    int32_t* mem = nullptr;
+    int32_t* cptr = nullptr;
+    int32_t* child = nullptr;
+    int32_t* key_sorted = nullptr;
+    int32_t* iota = nullptr;
+    int32_t* cnt = nullptr;
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+};
+
+size_t cub_tmp_bytes(int32_t n) {
+    return std::max(sort_temp_bytes_i32(n), scan_temp_bytes(n + 2)) + 256;
+}
+
+size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) {
+    const int32_t n_src = approx ? k : n;
+    RepulsePlan p = plan_repulse(n, n_src, dim);
+    size_t b = al((size_t)p.P * n * stride_of(dim) * sizeof(float));
+    (void)mean_row;
+    b += al((size_t)gather_blocks(n, 1e9) * 3 * sizeof(double));  // bound: G = 32
+    b += al(sizeof(int32_t) * 4);
+    if (approx) {
+        b += al((size_t)k * sizeof(float4)) + al((size_t)(k + 1) * 4) + al((size_t)n * 4);
+        b += al((size_t)(n + 1) * 4) + al((size_t)n * 4);
+        b += al((size_t)n * 4) * 2 + al((size_t)(std::max(n, k) + 2) * 4);
+        b += al(cub_tmp_bytes(n));
+    }
+    return b + 4096;
+}
+
+bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double mean_row, SweepBufs& sb) {
+    const int32_t n_src = approx ? k : n;
+    RepulsePlan p = plan_repulse(n, n_src, dim);
+    sb.part = cv.take<float>((size_t)p.P * n * stride_of(dim));
+    (void)mean_row;
+    sb.stat_partial = cv.take<double>((size_t)gather_blocks(n, 1e9) * 3);
+    sb.flags = cv.take<int32_t>(4);
+    if (approx) {
+        sb.reps = cv.take<float4>(k);
+        sb.mptr = cv.take<int32_t>(k + 1);
+        sb.mem = cv.take<int32_t>(n);
+        sb.cptr = cv.take<int32_t>(n + 1);
+        sb.child = cv.take<int32_t>(n);
+        sb.key_sorted = cv.take<int32_t>(n);
+        sb.iota = cv.take<int32_t>(n);
+        sb.cnt = cv.take<int32_t>(std::max(n, k) + 2);
+        sb.tmp_bytes = cub_tmp_bytes(n);
+        sb.tmp = cv.take<char>(sb.tmp_bytes);
+    }
+    return cv.ok;
+}
+
+// Group maps into CSRs (members of each representative, children of each parent).
+cudaError_t prepare_approx(int32_t n, const mm_approx* ap, SweepBufs& sb, cudaStream_t st) {
+    cudaError_t e = group_by_key(n, ap->ancestor, ap->k, sb.mptr, sb.mem, sb.key_sorted, sb.iota, sb.cnt, sb.tmp,
+                                 sb.tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    return group_by_key(n, ap->parent, n, sb.cptr, sb.child, sb.key_sorted, sb.iota, sb.cnt, sb.tmp, sb.tmp_bytes,
+                        st);
+}
+
+// One sweep with all buffers prepared (graph-capturable: no allocation, no sync).
+cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* x_in,
+                       float* x_out, mm_sweep_stats* stats, const SweepBufs& sb, cudaStream_t st) {
+    const int32_t n = S->n;
+    const double mean_row = (double)S->nnz / (double)n;
+    const bool qpow = q != 0.0f;
+    cudaError_t e;
+    RepulsePlan p;
+    if (ap) {
+        e = launch_centroid(dim, ap->k, sb.mptr, sb.mem, x_in, sb.reps, st);
+        if (e != cudaSuccess) return e;
+        p = plan_repulse(n, ap->k, dim);
+        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.reps, ap->ancestor, p, sb.part, st);
+    } else {
+        p = plan_repulse(n, n, dim);
+        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, p, sb.part, st);
+    }
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(sb.flags, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    GatherArgs ga;
+    ga.n = n;
+    ga.rp = S->row_ptr;
+    ga.col = S->col;
+    ga.d = S->d;
+    ga.w = S->w;
+    ga.x = x_in;
+    ga.alpha = alpha;
+    ga.q = q;
+    ga.part = sb.part;
+    ga.P = p.P;
+    ga.parent = ap ? ap->parent : nullptr;
+    ga.child_ptr = ap ? sb.cptr : nullptr;
+    ga.child = ap ? sb.child : nullptr;
+    ga.x_out = x_out;
+    ga.stat_partial = sb.stat_partial;
+    ga.flags = sb.flags;
+    e = launch_gather(dim, ga, mean_row, st);
+    if (e != cudaSuccess) return e;
+    if (stats) e = launch_stats_final(sb.stat_partial, gather_blocks(n, mean_row), sb.flags, stats, st);
+    return e;
+}
+
+// Energy with caller-provided stream; syncs.
+mm_status energy_core(const mm_sset* S, int dim, double alpha, double q, const float* x, double* out,
+                      cudaStream_t st) {
+    const int32_t n = S->n;
+    const double mean_row = (double)S->nnz / (double)n;
+    EntropyPlan ep = plan_entropy(n);
+    const int nb_all = ep.tblocks * ep.P, nb_s = gather_blocks(n, mean_row);
+    const size_t bytes = al((size_t)nb_all * 8) + al((size_t)nb_s * 16) + al(16);
+    DevBuf buf(bytes, st);
+    if (!buf.p) { set_err("mm_energy: out of device memory (%zu B)", bytes); return MM_ERR_OUT_OF_MEMORY; }
+    Carver cv(buf.p, bytes);
+    double* pa = cv.take<double>(nb_all);
+    double* ps = cv.take<double>((size_t)nb_s * 2);
+    int32_t* coinc = cv.take<int32_t>(4);
+    MM_CU(cudaMemsetAsync(coinc, 0, 16, st), "mm_energy memset");
+    MM_CU(launch_entropy_all(dim, q, n, x, ep, pa, coinc, st), "mm_energy entropy_all");
+    MM_CU(launch_energy_s(dim, q, n, S->row_ptr, S->col, S->d, S->w, x, mean_row, ps, coinc + 1, st),
+          "mm_energy energy_s");
+    std::vector<double> ha(nb_all), hs((size_t)nb_s * 2);
+    int32_t hc[2] = {0, 0};
+    MM_CU(cudaMemcpyAsync(ha.data(), pa, (size_t)nb_all * 8, cudaMemcpyDeviceToHost, st), "mm_energy d2h");
+    MM_CU(cudaMemcpyAsync(hs.data(), ps, (size_t)nb_s * 16, cudaMemcpyDeviceToHost, st), "mm_energy d2h");
+    MM_CU(cudaMemcpyAsync(hc, coinc, 8, cudaMemcpyDeviceToHost, st), "mm_energy d2h");
+    MM_CU(cudaStreamSynchronize(st), "mm_energy sync");
+    double sa = 0.0, ss = 0.0, sp = 0.0;
+    for (int b = 0; b < nb_all; ++b) sa += ha[b];
+    for (int b = 0; b < nb_s; ++b) {
+        ss += hs[(size_t)b * 2];
+        sp += hs[(size_t)b * 2 + 1];
+    }
+    const double diff = sa - sp;
+    const double entropy = (q == 0.0) ? 0.5 * (-0.5 * M_LN2) * diff : 0.5 * diff / q;
+    out[0] = 0.5 * ss;
+    out[1] = entropy;
+    out[2] = out[0] + alpha * out[1];
+    if (hc[0] > hc[1]) {
+        set_err("mm_energy: %d coincident non-S ordered pair(s): ln 0 is undefined (Eq.(1))", hc[0] - hc[1]);
+        return MM_ERR_NONFINITE;
+    }
+    if (!isfinite(out[2])) {
+        set_err("mm_energy: non-finite energy");
+        return MM_ERR_NONFINITE;
+    }
+    return MM_OK;
+}
+
+}  // namespace
+
+// ================================================================== C ABI
+extern "C" {
+
+const char* mm_status_string(mm_status s) {
+    switch (s) {
+        case MM_OK: return "MM_OK";
+        case MM_ERR_INVALID_ARGUMENT: return "MM_ERR_INVALID_ARGUMENT";
+        case MM_ERR_INVALID_INPUT: return "MM_ERR_INVALID_INPUT";
+        case MM_ERR_NONFINITE: return "MM_ERR_NONFINITE";
+        case MM_ERR_OUT_OF_MEMORY: return "MM_ERR_OUT_OF_MEMORY";
+        case MM_ERR_CUDA: return "MM_ERR_CUDA";
+        case MM_ERR_UNSUPPORTED: return "MM_ERR_UNSUPPORTED";
+    }
+    return "MM_ERR_UNKNOWN";
+}
+
+const char* mm_last_error(void) { return g_err.c_str(); }
+
+const char* mm_version(void) { return "mm_b200 0.1 sm_100a"; }
+
+mm_status mm_set_allocator(void* (*alloc)(size_t, mm_stream_t, void*), void (*free_)(void*, mm_stream_t, void*),
+                           void* ctx) {
+    if ((alloc == nullptr) != (free_ == nullptr)) {
+        set_err("mm_set_allocator: alloc and free must both be set or both be NULL");
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    g_alloc = alloc;
+    g_free = free_;
+    g_alloc_ctx = ctx;
+    return MM_OK;
+}
+
+mm_status mm_sweep_workspace(int32_t n, int dim, const mm_approx* ap, size_t* bytes) {
+    if (!bytes || n <= 0) { set_err("mm_sweep_workspace: bad arguments"); return MM_ERR_INVALID_ARGUMENT; }
+    if (dim != 2 && dim != 3) { set_err("mm_sweep_workspace: dim must be 2 or 3"); return MM_ERR_UNSUPPORTED; }
+    if (ap && ap->k <= 0) { set_err("mm_sweep_workspace: ap->k must be > 0"); return MM_ERR_INVALID_ARGUMENT; }
+    *bytes = sweep_bytes(n, dim, ap ? ap->k : 0, ap != nullptr, 1.0);
+    return MM_OK;
+}
+
+mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* x_in,
+                   float* x_out, mm_sweep_stats* stats, void* ws, size_t ws_bytes, mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_sset(S, "mm_sweep")) != MM_OK) return s;
+    if ((s = check_dim_q(dim, q, "mm_sweep")) != MM_OK) return s;
+    if ((s = check_x(x_in, dim, "x_in", "mm_sweep")) != MM_OK) return s;
+    if ((s = check_x(x_out, dim, "x_out", "mm_sweep")) != MM_OK) return s;
+    if (!isfinite(alpha)) { set_err("mm_sweep: alpha must be finite"); return MM_ERR_INVALID_ARGUMENT; }
+    const int32_t n = S->n;
+    const size_t xb = (size_t)n * stride_of(dim) * sizeof(float);
+    const char *a0 = (const char*)x_in, *b0 = (const char*)x_out;
+    if (a0 < b0 + xb && b0 < a0 + xb) { set_err("mm_sweep: x_out must not alias x_in"); return MM_ERR_INVALID_ARGUMENT; }
+    if (ap) {
+        if (ap->k <= 0 || ap->k > n || !ap->parent || !ap->ancestor) {
+            set_err("mm_sweep: bad mm_approx (k=%d must be in [1, n], maps non-NULL)", ap ? ap->k : 0);
+            return MM_ERR_INVALID_ARGUMENT;
+        }
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const double mean_row = (double)S->nnz / (double)n;
+    const size_t need = sweep_bytes(n, dim, ap ? ap->k : 0, ap != nullptr, mean_row);
+    DevBuf own;
+    void* base = ws;
+    size_t cap = ws_bytes;
+    if (!ws) {
+        own.st = st;
+        own.p = dev_alloc(need, st);
+        if (!own.p) { set_err("mm_sweep: out of device memory (%zu B)", need); return MM_ERR_OUT_OF_MEMORY; }
+        base = own.p;
+        cap = need;
+    } else if (ws_bytes < need) {
+        set_err("mm_sweep: workspace too small (%zu < %zu B)", ws_bytes, need);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    Carver cv(base, cap);
+    SweepBufs sb;
+    if (!carve_sweep(cv, n, dim, ap ? ap->k : 0, ap != nullptr, mean_row, sb)) {
+        set_err("mm_sweep: workspace carving failed");
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    if (ap) MM_CU(prepare_approx(n, ap, sb, st), "mm_sweep prepare_approx");
+    MM_CU(sweep_core(S, dim, alpha, q, ap, x_in, x_out, stats, sb, st), "mm_sweep");
+    return MM_OK;
+}
+
+mm_status mm_energy(const mm_sset* S, int dim, double alpha, double q, const float* x, double* out,
+                    mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_sset(S, "mm_energy")) != MM_OK) return s;
+    if ((s = check_dim_q(dim, q, "mm_energy")) != MM_OK) return s;
+    if ((s = check_x(x, dim, "x", "mm_energy")) != MM_OK) return s;
+    if (!out) { set_err("mm_energy: out is NULL"); return MM_ERR_INVALID_ARGUMENT; }
+    return energy_core(S, dim, alpha, q, x, out, (cudaStream_t)stream);
+}
+
+int64_t mm_launch_count(void) { return g_launches.load(); }
+
+mm_status mm_profile_enable(int on) {
+    g_prof_on.store(on ? 1 : 0);
+    return MM_OK;
+}
+
+mm_status mm_profile_reset(void) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto& p : g_pending) {
+        cudaEventSynchronize(p.b);
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g_pending.clear();
+    g_prof.clear();
+    return MM_OK;
+}
+
+mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    for (auto& p : g_pending) {
+        cudaError_t e = cudaEventSynchronize(p.b);
+        float ms = 0.f;
+        if (e == cudaSuccess && cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+            auto& r = g_prof[p.name];
+            r.first += 1;
+            r.second += ms;
+        } else {
+            cudaGetLastError();
+        }
+        cudaEventDestroy(p.a);
+        cudaEventDestroy(p.b);
+    }
+    g_pending.clear();
+    int32_t i = 0;
+    for (auto& kv : g_prof) {
+        if (out && i < max) {
+            memset(out[i].name, 0, sizeof(out[i].name));
+            strncpy(out[i].name, kv.first.c_str(), sizeof(out[i].name) - 1);
+            out[i].launches = kv.second.first;
+            out[i].total_ms = kv.second.second;
+        }
+        ++i;
+    }
+    if (count) *count = i;
+    return MM_OK;
+}
+
+}  // extern "C"
+
+// ================================================================== hierarchy
+struct HLevel {
+    int32_t n = 0;
+    int64_t nnz = 0;
+    int64_t* rp = nullptr;
+    int32_t* col = nullptr;
+    int32_t* omega = nullptr;
+    int32_t* c = nullptr;
+    int32_t* parent = nullptr;
+    float* d = nullptr;
+    float* w = nullptr;
+    int32_t rounds = 0;
+};
+
+struct mm_hierarchy {
+    std::vector<HLevel> lv;
+};
+
+namespace {
+
+void free_level(HLevel& l) {
+    dev_free(l.rp, nullptr);
+    dev_free(l.col, nullptr);
+    dev_free(l.omega, nullptr);
+    dev_free(l.c, nullptr);
+    dev_free(l.parent, nullptr);
+    dev_free(l.d, nullptr);
+    dev_free(l.w, nullptr);
+    l = HLevel();
+}
+
+template <class T>
+T* alloc_n(size_t count, cudaStream_t st) {
+    return (T*)dev_alloc(sizeof(T) * (count > 0 ? count : 1), st);
+}
+
+mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uint64_t seed, int32_t n_stop,
+                               int32_t max_levels, int32_t max_rounds, mm_hierarchy** out, cudaStream_t st) {
+    const int32_t n0 = g->n;
+    const int64_t nnz0 = g->nnz;
+    mm_hierarchy* H = new mm_hierarchy();
+    auto fail = [&](mm_status s) {
+        cudaStreamSynchronize(st);
+        for (auto& l : H->lv) free_level(l);
+        delete H;
+        return s;
+    };
+    HLevel l0;
+    l0.n = n0;
+    l0.nnz = nnz0;
+    l0.rp = alloc_n<int64_t>((size_t)n0 + 1, st);
+    l0.col = alloc_n<int32_t>(nnz0, st);
+    l0.omega = alloc_n<int32_t>(nnz0, st);
+    l0.c = alloc_n<int32_t>(n0, st);
+    H->lv.push_back(l0);
+    if (!l0.rp || !l0.col || !l0.omega || !l0.c) { set_err("mm_build_hierarchy: out of memory"); return fail(MM_ERR_OUT_OF_MEMORY); }
+    if (cudaMemcpyAsync(l0.rp, g->row_ptr, sizeof(int64_t) * ((size_t)n0 + 1), cudaMemcpyDeviceToDevice, st) ||
+        (nnz0 > 0 && cudaMemcpyAsync(l0.col, g->col, sizeof(int32_t) * nnz0, cudaMemcpyDeviceToDevice, st))) {
+        set_err("mm_build_hierarchy: copy failed");
+        return fail(MM_ERR_CUDA);
+    }
+    if (g->omega) {
+        if (nnz0 > 0 && cudaMemcpyAsync(l0.omega, g->omega, sizeof(int32_t) * nnz0, cudaMemcpyDeviceToDevice, st)) {
+            set_err("mm_build_hierarchy: copy failed");
+            return fail(MM_ERR_CUDA);
+        }
+    } else if (launch_fill(nnz0, 1, l0.omega, st) != cudaSuccess) {
+        set_err("mm_build_hierarchy: fill failed");
+        return fail(MM_ERR_CUDA);
+    }
+    if (c) {
+        if (cudaMemcpyAsync(l0.c, c, sizeof(int32_t) * n0, cudaMemcpyDeviceToDevice, st)) {
+            set_err("mm_build_hierarchy: copy failed");
+            return fail(MM_ERR_CUDA);
+        }
+    } else if (launch_fill(n0, 1, l0.c, st) != cudaSuccess) {
+        set_err("mm_build_hierarchy: fill failed");
+        return fail(MM_ERR_CUDA);
+    }
+    // scratch sized by level 0 (levels only shrink)
+    const int64_t m0 = std::max<int64_t>(nnz0, 1);
+    const size_t tmpb = std::max(sort_temp_bytes_u64(m0), scan_temp_bytes((int32_t)std::max<int64_t>(m0, n0 + 2))) + 256;
+    const size_t bytes = al((size_t)n0 * 4) * 6 + al(64) + al((size_t)m0 * 8) * 2 + al((size_t)m0 * 4) * 6 +
+                         al(((size_t)n0 + 2) * 4) * 2 + al(tmpb) + 4096;
+    DevBuf scratch(bytes, st);
+    if (!scratch.p) { set_err("mm_build_hierarchy: out of memory (%zu B scratch)", bytes); return fail(MM_ERR_OUT_OF_MEMORY); }
+    Carver cv(scratch.p, bytes);
+    int32_t* mate = cv.take<int32_t>(n0);
+    int32_t* cand = cv.take<int32_t>(n0);
+    int32_t* flag = cv.take<int32_t>(n0);
+    int32_t* cid = cv.take<int32_t>(n0);
+    int32_t* cnext = cv.take<int32_t>(n0);
+    int32_t* spare = cv.take<int32_t>(n0);
+    (void)spare;
+    int32_t* added = cv.take<int32_t>(16);
+    uint64_t* keys = cv.take<uint64_t>(m0);
+    uint64_t* keys_alt = cv.take<uint64_t>(m0);
+    int32_t* vals = cv.take<int32_t>(m0);
+    int32_t* vals_alt = cv.take<int32_t>(m0);
+    int32_t* head = cv.take<int32_t>(m0);
+    int32_t* pos = cv.take<int32_t>(m0);
+    int32_t* ccol = cv.take<int32_t>(m0);
+    int32_t* comega = cv.take<int32_t>(m0);
+    int32_t* rowcnt = cv.take<int32_t>((size_t)n0 + 2);
+    int32_t* excl = cv.take<int32_t>((size_t)n0 + 2);
+    void* tmp = cv.take<char>(tmpb);
+    if (!cv.ok) { set_err("mm_build_hierarchy: scratch carving failed"); return fail(MM_ERR_INVALID_ARGUMENT); }
+
+    while ((int32_t)H->lv.size() < max_levels) {
+        const size_t li = H->lv.size() - 1;
+        const HLevel cur = H->lv[li];
+        if (cur.n <= n_stop) break;
+        if (launch_fill(cur.n, -1, mate, st) != cudaSuccess) { set_err("mm_build_hierarchy: fill"); return fail(MM_ERR_CUDA); }
+        int32_t rounds = max_rounds;
+        for (int32_t r = 0; r < max_rounds; ++r) {
+            int32_t h_added = 0;
+            if (cudaMemsetAsync(added, 0, 4, st) ||
+                run_match_round(cur.n, cur.rp, cur.col, cur.omega, cur.c, mate, cand, seed, (int32_t)li, r, added, st) ||
+                cudaMemcpyAsync(&h_added, added, 4, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st)) {
+                cudaError_t e = cudaGetLastError();
+                set_err("mm_build_hierarchy: matching round failed: %s", cudaGetErrorString(e));
+                return fail(MM_ERR_CUDA);
+            }
+            if (h_added == 0) {
+                rounds = r + 1;
+                break;
+            }
+        }
+        H->lv[li].rounds = rounds;
+        int32_t* parent = alloc_n<int32_t>(cur.n, st);
+        if (!parent) { set_err("mm_build_hierarchy: out of memory"); return fail(MM_ERR_OUT_OF_MEMORY); }
+        int32_t last[2] = {0, 0};
+        if (contract_leaders(cur.n, mate, cur.c, flag, cid, parent, cnext, tmp, tmpb, st) ||
+            cudaMemcpyAsync(&last[0], cid + cur.n - 1, 4, cudaMemcpyDeviceToHost, st) ||
+            cudaMemcpyAsync(&last[1], flag + cur.n - 1, 4, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st)) {
+            dev_free(parent, st);
+            set_err("mm_build_hierarchy: contraction failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return fail(MM_ERR_CUDA);
+        }
+        const int32_t nc = last[0] + last[1];
+        if ((int64_t)10 * nc > (int64_t)9 * cur.n) {  // Q17: less than 10% smaller -> discard, stop
+            dev_free(parent, st);
+            break;
+        }
+        int64_t m2 = 0;
+        if (cur.nnz > 0) {
+            int32_t lastp[2] = {0, 0};
+            if (contract_edges(cur.n, cur.nnz, cur.rp, cur.col, cur.omega, parent, nc, keys, keys_alt, vals, vals_alt,
+                               head, pos, ccol, comega, rowcnt, tmp, tmpb, st) ||
+                cudaMemcpyAsync(&lastp[0], pos + cur.nnz - 1, 4, cudaMemcpyDeviceToHost, st) ||
+                cudaMemcpyAsync(&lastp[1], head + cur.nnz - 1, 4, cudaMemcpyDeviceToHost, st) ||
+                cudaStreamSynchronize(st)) {
+                dev_free(parent, st);
+                set_err("mm_build_hierarchy: edge contraction failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return fail(MM_ERR_CUDA);
+            }
+            m2 = (int64_t)lastp[0] + lastp[1];
+        } else if (launch_fill(nc + 1, 0, rowcnt, st) != cudaSuccess) {
+            dev_free(parent, st);
+            set_err("mm_build_hierarchy: fill failed");
+            return fail(MM_ERR_CUDA);
+        }
+        HLevel nx;
+        nx.n = nc;
+        nx.nnz = m2;
+        nx.rp = alloc_n<int64_t>((size_t)nc + 1, st);
+        nx.col = alloc_n<int32_t>(m2, st);
+        nx.omega = alloc_n<int32_t>(m2, st);
+        nx.c = alloc_n<int32_t>(nc, st);
+        nx.d = alloc_n<float>(m2, st);
+        nx.w = alloc_n<float>(m2, st);
+        H->lv[li].parent = parent;
+        H->lv.push_back(nx);
+        if (!nx.rp || !nx.col || !nx.omega || !nx.c || !nx.d || !nx.w) {
+            set_err("mm_build_hierarchy: out of memory");
+            return fail(MM_ERR_OUT_OF_MEMORY);
+        }
+        if (rowptr_from_counts(nc, rowcnt, excl, m2, nx.rp, tmp, tmpb, st) ||
+            (m2 > 0 && cudaMemcpyAsync(nx.col, ccol, 4 * m2, cudaMemcpyDeviceToDevice, st)) ||
+            (m2 > 0 && cudaMemcpyAsync(nx.omega, comega, 4 * m2, cudaMemcpyDeviceToDevice, st)) ||
+            cudaMemcpyAsync(nx.c, cnext, 4 * (size_t)nc, cudaMemcpyDeviceToDevice, st) ||
+            launch_coarse_sset(nc, nx.rp, nx.col, nx.c, dim, nx.d, nx.w, st)) {
+            set_err("mm_build_hierarchy: level assembly failed: %s", cudaGetErrorString(cudaGetLastError()));
+            return fail(MM_ERR_CUDA);
+        }
+    }
+    if (cudaStreamSynchronize(st) != cudaSuccess) {
+        set_err("mm_build_hierarchy: %s", cudaGetErrorString(cudaGetLastError()));
+        return fail(MM_ERR_CUDA);
+    }
+    *out = H;
+    return MM_OK;
+}
+
+mm_status check_graph(const mm_graph* g, const char* who) {
+    if (!g || g->n <= 0 || g->nnz < 0 || !g->row_ptr || (g->nnz > 0 && !g->col)) {
+        set_err("%s: bad mm_graph (n > 0, nnz >= 0, row_ptr/col non-NULL required)", who);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    if (g->nnz > INT32_MAX) { set_err("%s: nnz > 2^31-1 unsupported", who); return MM_ERR_UNSUPPORTED; }
+    return MM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+mm_status mm_build_hierarchy(const mm_graph* g, const int32_t* c, int dim, uint64_t seed, int32_t n_stop,
+                             int32_t max_levels, int32_t max_rounds, mm_hierarchy** out, mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_graph(g, "mm_build_hierarchy")) != MM_OK) return s;
+    if (dim != 2 && dim != 3) { set_err("mm_build_hierarchy: dim must be 2 or 3"); return MM_ERR_UNSUPPORTED; }
+    if (!out || n_stop < 1 || max_levels < 1 || max_levels > MM_MAX_LEVELS || max_rounds < 1) {
+        set_err("mm_build_hierarchy: bad arguments (out non-NULL, n_stop >= 1, 1 <= max_levels <= %d, max_rounds >= 1)",
+                MM_MAX_LEVELS);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    return build_hierarchy_impl(g, c, dim, seed, n_stop, max_levels, max_rounds, out, (cudaStream_t)stream);
+}
+
+int32_t mm_hierarchy_num_levels(const mm_hierarchy* h) { return h ? (int32_t)h->lv.size() : 0; }
+
+mm_status mm_hierarchy_level(const mm_hierarchy* h, int32_t level, mm_level_view* out) {
+    if (!h || !out || level < 0 || level >= (int32_t)h->lv.size()) {
+        set_err("mm_hierarchy_level: bad arguments");
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    const HLevel& l = h->lv[level];
+    out->n = l.n;
+    out->nnz = l.nnz;
+    out->row_ptr = l.rp;
+    out->col = l.col;
+    out->omega = l.omega;
+    out->c = l.c;
+    out->parent = l.parent;
+    out->d = l.d;
+    out->w = l.w;
+    out->rounds = l.rounds;
+    return MM_OK;
+}
+
+mm_status mm_hierarchy_copy_level(const mm_hierarchy* h, int32_t level, int64_t* row_ptr, int32_t* col,
+                                  int32_t* omega, int32_t* c, int32_t* parent, float* d, float* w, mm_stream_t stream) {
+    if (!h || level < 0 || level >= (int32_t)h->lv.size()) {
+        set_err("mm_hierarchy_copy_level: bad arguments");
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    const HLevel& l = h->lv[level];
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto cp = [&](void* dst, const void* src, size_t bytes) {
+        return (dst && src && bytes) ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) : cudaSuccess;
+    };
+    MM_CU(cp(row_ptr, l.rp, sizeof(int64_t) * ((size_t)l.n + 1)), "mm_hierarchy_copy_level");
+    MM_CU(cp(col, l.col, sizeof(int32_t) * l.nnz), "mm_hierarchy_copy_level");
+    MM_CU(cp(omega, l.omega, sizeof(int32_t) * l.nnz), "mm_hierarchy_copy_level");
+    MM_CU(cp(c, l.c, sizeof(int32_t) * l.n), "mm_hierarchy_copy_level");
+    MM_CU(cp(parent, l.parent, sizeof(int32_t) * l.n), "mm_hierarchy_copy_level");
+    MM_CU(cp(d, l.d, sizeof(float) * l.nnz), "mm_hierarchy_copy_level");
+    MM_CU(cp(w, l.w, sizeof(float) * l.nnz), "mm_hierarchy_copy_level");
+    MM_CU(cudaStreamSynchronize(st), "mm_hierarchy_copy_level");
+    return MM_OK;
+}
+
+void mm_hierarchy_free(mm_hierarchy* h) {
+    if (!h) return;
+    cudaDeviceSynchronize();
+    for (auto& l : h->lv) free_level(l);
+    delete h;
+}
+
+}  // extern "C"
+
+// ================================================================== layout driver
+namespace {
+
+bool graphs_enabled() {
+    const char* e = getenv("MM_NO_GRAPHS");
+    return !(e && e[0] && e[0] != '0') && !g_prof_on.load();
+}
+
+// Runs K sweeps ping-ponging between bufA/bufB starting from src; returns the
+// buffer holding the result.  Optionally captured into one CUDA graph.
+cudaError_t run_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* src,
+                       float* bufA, float* bufB, int32_t K, mm_sweep_stats* stats, const SweepBufs& sb,
+                       cudaStream_t st, const float** result) {
+    if (K <= 0) {
+        *result = src;
+        return cudaSuccess;
+    }
+    const bool use_graph = graphs_enabled() && K > 1;
+    cudaGraph_t graph = nullptr;
+    if (use_graph) {
+        cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return e;
+    }
+    const float* cur = src;
+    cudaError_t err = cudaSuccess;
+    for (int32_t s = 0; s < K && err == cudaSuccess; ++s) {
+        float* dst = (cur == bufA) ? bufB : bufA;
+        err = sweep_core(S, dim, alpha, q, ap, cur, dst, stats, sb, st);
+        cur = dst;
+    }
+    if (use_graph) {
+        cudaError_t e = cudaStreamEndCapture(st, &graph);
+        if (err == cudaSuccess) err = e;
+        if (err == cudaSuccess) {
+            cudaGraphExec_t exec = nullptr;
+            err = cudaGraphInstantiate(&exec, graph, 0);
+            if (err == cudaSuccess) err = cudaGraphLaunch(exec, st);
+            if (err == cudaSuccess) err = cudaStreamSynchronize(st);
+            if (exec) cudaGraphExecDestroy(exec);
+        }
+        if (graph) cudaGraphDestroy(graph);
+    }
+    *result = cur;
+    return err;
+}
+
+}  // namespace
+
+extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, float alpha, float q, int h,
+                               const int32_t* sweeps, int32_t nsweeps, uint64_t seed, int32_t n_stop,
+                               const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_sset(S, "mm_layout")) != MM_OK) return s;
+    if ((s = check_dim_q(dim, q, "mm_layout")) != MM_OK) return s;
+    if ((s = check_x(x_out, dim, "x_out", "mm_layout")) != MM_OK) return s;
+    if (!sweeps || nsweeps < 1 || h < 0 || !isfinite(alpha)) {
+        set_err("mm_layout: bad arguments (sweeps host array with nsweeps >= 1, h >= 0, finite alpha)");
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    for (int32_t t = 0; t < nsweeps; ++t)
+        if (sweeps[t] < 0) { set_err("mm_layout: negative sweep count"); return MM_ERR_INVALID_ARGUMENT; }
+    if (h == 0 && (s = check_x(x_init, dim, "x_init", "mm_layout")) != MM_OK) return s;
+    if (h > 0) {
+        if ((s = check_graph(g, "mm_layout")) != MM_OK) return s;
+        if (g->n != S->n) { set_err("mm_layout: graph and S sizes differ"); return MM_ERR_INVALID_ARGUMENT; }
+        if (n_stop < 1) { set_err("mm_layout: n_stop must be >= 1"); return MM_ERR_INVALID_ARGUMENT; }
+    }
+    const int32_t n0 = S->n;
+    const int st_w = stride_of(dim);
+    const size_t xbytes = (size_t)n0 * st_w * sizeof(float);
+    cudaStream_t us = (cudaStream_t)stream;
+    cudaStream_t ls = nullptr;
+    cudaEvent_t ev = nullptr;
+    MM_CU(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking), "mm_layout stream");
+    struct StreamGuard {
+        cudaStream_t s;
+        cudaEvent_t e;
+        ~StreamGuard() {
+            if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+            if (e) cudaEventDestroy(e);
+        }
+    } guard{ls, nullptr};
+    MM_CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "mm_layout event");
+    guard.e = ev;
+    MM_CU(cudaEventRecord(ev, us), "mm_layout event");
+    MM_CU(cudaStreamWaitEvent(ls, ev, 0), "mm_layout wait");
+
+    mm_layout_report R;
+    memset(&R, 0, sizeof(R));
+    const auto K_of = [&](int32_t l) { return sweeps[std::min(l, nsweeps - 1)]; };
+
+    if (h == 0) {
+        const int32_t K = K_of(0);
+        const double mean_row = (double)S->nnz / n0;
+        const size_t need = sweep_bytes(n0, dim, 0, false, mean_row) + al(xbytes) + al(sizeof(mm_sweep_stats));
+        DevBuf buf(need, ls);
+        if (!buf.p) { set_err("mm_layout: out of device memory (%zu B)", need); return MM_ERR_OUT_OF_MEMORY; }
+        Carver cv(buf.p, need);
+        float* tmpx = cv.take<float>((size_t)n0 * st_w);
+        mm_sweep_stats* dstats = cv.take<mm_sweep_stats>(1);
+        SweepBufs sb;
+        if (!carve_sweep(cv, n0, dim, 0, false, mean_row, sb)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+        MM_CU(cudaMemsetAsync(dstats, 0, sizeof(mm_sweep_stats), ls), "mm_layout memset");
+        // choose the first destination so that the last sweep lands in x_out
+        const float* src = x_init;
+        float *A, *B;
+        const char *pi = (const char*)x_init, *po = (const char*)x_out;
+        if (pi == po) {  // in-place request: iterate from a copy (Jacobi needs two buffers)
+            MM_CU(cudaMemcpyAsync(tmpx, x_init, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
+            src = tmpx;
+            A = x_out;
+            B = tmpx;
+        } else if (pi < po + xbytes && po < pi + xbytes) {
+            set_err("mm_layout: x_init partially overlaps x_out");
+            return MM_ERR_INVALID_ARGUMENT;
+        } else {
+            A = (K % 2 == 1) ? x_out : tmpx;
+            B = (A == x_out) ? tmpx : x_out;
+        }
+        const float* res = nullptr;
+        MM_CU(run_sweeps(S, dim, alpha, q, nullptr, src, A, B, K, dstats, sb, ls, &res), "mm_layout sweeps");
+        if (res != x_out) MM_CU(cudaMemcpyAsync(x_out, res, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
+        mm_sweep_stats hs;
+        MM_CU(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, ls), "mm_layout d2h");
+        MM_CU(cudaStreamSynchronize(ls), "mm_layout sync");
+        R.levels = 1;
+        R.n_level[0] = n0;
+        R.rel_change = hs.x2 > 0 ? sqrt(hs.dx2 / hs.x2) : INFINITY;
+        R.vertex_updates = (int64_t)n0 * K;
+        R.pair_interactions = (int64_t)n0 * (n0 - 1) * K;
+        if (hs.flags & 1) { set_err("mm_layout: non-finite coordinate produced"); return MM_ERR_NONFINITE; }
+    } else {
+        mm_hierarchy* H = nullptr;
+        if ((s = build_hierarchy_impl(g, nullptr, dim, seed, n_stop, MM_MAX_LEVELS, 64, &H, ls)) != MM_OK) return s;
+        struct HGuard {
+            mm_hierarchy* h;
+            ~HGuard() { mm_hierarchy_free(h); }
+        } hg{H};
+        const int32_t nl = (int32_t)H->lv.size(), L = nl - 1;
+        R.levels = nl;
+        auto S_of = [&](int32_t l) {
+            mm_sset t;
+            if (l == 0) return *S;
+            t.n = H->lv[l].n;
+            t.nnz = H->lv[l].nnz;
+            t.row_ptr = H->lv[l].rp;
+            t.col = H->lv[l].col;
+            t.d = H->lv[l].d;
+            t.w = H->lv[l].w;
+            return t;
+        };
+        // workspace = max over levels
+        size_t wsb = 0;
+        for (int32_t l = 0; l <= L; ++l) {
+            const int32_t hp = std::min(h, L - l);
+            const int32_t k = (l == L) ? 0 : H->lv[l + hp].n;
+            wsb = std::max(wsb, sweep_bytes(H->lv[l].n, dim, k, l != L, 1.0));
+        }
+        const size_t need = wsb + 2 * al(xbytes) + 2 * al((size_t)n0 * 4) + al(sizeof(mm_sweep_stats)) + al(64);
+        DevBuf buf(need, ls);
+        if (!buf.p) { set_err("mm_layout: out of device memory (%zu B)", need); return MM_ERR_OUT_OF_MEMORY; }
+        Carver cv(buf.p, need);
+        float* xa = cv.take<float>((size_t)n0 * st_w);
+        float* xb = cv.take<float>((size_t)n0 * st_w);
+        int32_t* anc = cv.take<int32_t>(n0);
+        int32_t* anc2 = cv.take<int32_t>(n0);
+        mm_sweep_stats* dstats = cv.take<mm_sweep_stats>(1);
+        double* dsum = cv.take<double>(8);
+        const size_t ws_off = cv.off;
+        MM_CU(cudaMemsetAsync(dstats, 0, sizeof(mm_sweep_stats), ls), "mm_layout memset");
+        // coarsest level: box init + exact sweeps (Q13, Q14)
+        {
+            mm_sset SL = S_of(L);
+            const int32_t nL = SL.n;
+            MM_CU(launch_init_box(dim, nL, SL.d, SL.nnz, dsum, seed, L, xa, ls), "mm_layout init");
+            Carver wc((char*)buf.p + ws_off, need - ws_off);
+            SweepBufs sb;
+            if (!carve_sweep(wc, nL, dim, 0, false, 1.0, sb)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+            const float* res = nullptr;
+            MM_CU(run_sweeps(&SL, dim, alpha, q, nullptr, xa, xb, xa, K_of(L), dstats, sb, ls, &res), "mm_layout coarsest");
+            R.n_level[L] = nL;
+            R.k_level[L] = 0;
+            R.vertex_updates += (int64_t)nL * K_of(L);
+            R.pair_interactions += (int64_t)nL * (nL - 1) * K_of(L);
+            const float* cur = res;
+            for (int32_t l = L - 1; l >= 0; --l) {
+                const int32_t nf = H->lv[l].n;
+                float* dst = (cur == xa) ? xb : xa;
+                MM_CU(launch_prolong(dim, nf, H->lv[l].parent, cur, seed, l, dst, ls), "mm_layout prolong");
+                cur = dst;
+                const int32_t hp = std::min(h, L - l);
+                // H = parent_{l+hp-1} o ... o parent_l
+                MM_CU(cudaMemcpyAsync(anc, H->lv[l].parent, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, ls), "mm_layout anc");
+                for (int32_t t = 1; t < hp; ++t) {
+                    MM_CU(launch_compose(nf, anc, H->lv[l + t].parent, anc2, ls), "mm_layout compose");
+                    std::swap(anc, anc2);
+                }
+                mm_approx ap;
+                ap.k = H->lv[l + hp].n;
+                ap.parent = H->lv[l].parent;
+                ap.ancestor = anc;
+                mm_sset Sl = S_of(l);
+                Carver wl((char*)buf.p + ws_off, need - ws_off);
+                SweepBufs sbl;
+                if (!carve_sweep(wl, nf, dim, ap.k, true, 1.0, sbl)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+                MM_CU(prepare_approx(nf, &ap, sbl, ls), "mm_layout prepare_approx");
+                float* other = (cur == xa) ? xb : xa;
+                MM_CU(run_sweeps(&Sl, dim, alpha, q, &ap, cur, other, (float*)cur, K_of(l), dstats, sbl, ls, &res),
+                      "mm_layout sweeps");
+                cur = res;
+                R.n_level[l] = nf;
+                R.k_level[l] = ap.k;
+                R.vertex_updates += (int64_t)nf * K_of(l);
+                R.pair_interactions += ((int64_t)nf * (ap.k - 1) + 2 * (int64_t)(nf - H->lv[l + 1].n)) * K_of(l);
+            }
+            MM_CU(cudaMemcpyAsync(x_out, cur, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
+        }
+        mm_sweep_stats hs;
+        MM_CU(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, ls), "mm_layout d2h");
+        MM_CU(cudaStreamSynchronize(ls), "mm_layout sync");
+        R.rel_change = hs.x2 > 0 ? sqrt(hs.dx2 / hs.x2) : INFINITY;
+        if (hs.flags & 1) { set_err("mm_layout: non-finite coordinate produced"); return MM_ERR_NONFINITE; }
+    }
+    double en[3] = {0, 0, 0};
+    s = energy_core(S, dim, alpha, q, x_out, en, ls);
+    R.stress = en[0];
+    R.entropy = en[1];
+    R.energy = en[2];
+    if (rep) *rep = R;
+    // the caller's stream observes x_out only after our private stream finished
+    MM_CU(cudaEventRecord(ev, ls), "mm_layout event");
+    MM_CU(cudaStreamWaitEvent(us, ev, 0), "mm_layout wait");
+    return s;
+}

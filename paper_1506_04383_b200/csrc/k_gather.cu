@@ -1,0 +1,316 @@
+// k_gather.cu — kernel (a): S_i gather + position update, with the fused
+// convergence/stress reduction (e); and the S-part of mm_energy.
+//
+// For every vertex i (Eq.(2); Eq.(3)):
+//   rho_i = sum_{j in S_i} w_ij
+//   A_i   = sum_{j in S_i} w_ij (x_j + d_ij (x_i - x_j)/|x_i - x_j|)
+//   C_i   = sum_{j in S_i} r(i,j)            (removed from the all-pairs /
+//                                             representative sum: "subtracts
+//                                             values of r for {u,v} in E that
+//                                             have been added in good faith")
+//   Sib_i = sum_{j != i, P(j) = P(i)} r(i,j)  (Eq.(3) same-cluster term; approx only)
+//   R_i   = sum_p part[p][i] + Sib_i - C_i     (fixed order p = 0..P-1)
+//   x'_i  = (A_i + alpha R_i) / rho_i
+// with r(i,j) = (x_i - x_j)/|x_i - x_j|^(q+2) evaluated with exactly the same
+// FP32 operation sequence as kernels (b)/(c) so that the S-pair terms cancel
+// to rounding.  Synchronous (Jacobi): reads x, writes x_out.
+//
+// Mapping: a group of G lanes (G in {4,8,16,32}, chosen from the mean row
+// length) owns one vertex; lanes stride the CSR row so the col/d/w loads of a
+// group are contiguous; neighbour coordinates are 8/16-byte gathers (L2
+// resident for every config: x is at most 32 MB).  Group results are combined
+// with shuffles; per-CTA FP64 partials of |x'-x|^2, |x|^2 and the stress are
+// written for a fixed-order final reduction (relative change).
+#include "k_repulse.cuh"
+
+namespace mm {
+
+namespace {
+
+constexpr int kGBlock = 256;
+
+template <int G>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o, G);
+    return v;
+}
+
+template <int DIM, bool QPOW>
+__device__ __forceinline__ void r_value(const float4& xi, const float4& xj, float cexp, float4& acc, float sgn) {
+    const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+    float r2 = fmaf(dx, dx, kEps2);
+    r2 = fmaf(dy, dy, r2);
+    float dz = 0.f;
+    if constexpr (DIM == 3) {
+        dz = xi.z - xj.z;
+        r2 = fmaf(dz, dz, r2);
+    }
+    const float inv = inv_pow<QPOW>(r2, cexp) * sgn;
+    acc.x = fmaf(dx, inv, acc.x);
+    acc.y = fmaf(dy, inv, acc.y);
+    if constexpr (DIM == 3) acc.z = fmaf(dz, inv, acc.z);
+}
+
+template <int DIM, bool QPOW, int G>
+__global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
+    const int lg = threadIdx.x & (G - 1);
+    const int64_t i = ((int64_t)blockIdx.x * kGBlock + threadIdx.x) / G;
+    double v_dx2 = 0.0, v_x2 = 0.0, v_st = 0.0;
+    const bool valid = i < a.n;
+    float4 xi = make_float4(0.f, 0.f, 0.f, 0.f);
+    float rho = 0.f, st = 0.f;
+    float4 A = make_float4(0.f, 0.f, 0.f, 0.f), C = A;
+    if (valid) {
+        xi = load_x<DIM>(a.x, i);
+        const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];
+        for (int64_t e = e0 + lg; e < e1; e += G) {
+            const int32_t j = __ldg(a.col + e);
+            const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);
+            const float4 xj = load_x<DIM>(a.x, j);
+            const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+            float r2 = fmaf(dx, dx, kEps2);
+            r2 = fmaf(dy, dy, r2);
+            float dz = 0.f;
+            if constexpr (DIM == 3) {
+                dz = xi.z - xj.z;
+                r2 = fmaf(dz, dz, r2);
+            }
+            // S-pair r-value, removed from the all-pairs / representative sum
+            const float inv = inv_pow<QPOW>(r2, cexp);
+            C.x = fmaf(dx, inv, C.x);
+            C.y = fmaf(dy, inv, C.y);
+            if constexpr (DIM == 3) C.z = fmaf(dz, inv, C.z);
+            // attraction: w (x_j + d (x_i - x_j)/|x_i - x_j|)
+            const float rinv = rsqrt_approx(r2);
+            const float dist = r2 * rinv;
+            const float s = dd * rinv;
+            rho += ww;
+            A.x = fmaf(ww, fmaf(s, dx, xj.x), A.x);
+            A.y = fmaf(ww, fmaf(s, dy, xj.y), A.y);
+            if constexpr (DIM == 3) A.z = fmaf(ww, fmaf(s, dz, xj.z), A.z);
+            const float dev = dist - dd;
+            st = fmaf(ww * dev, dev, st);
+        }
+        if (a.parent != nullptr) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
+            const int32_t p = __ldg(a.parent + i);
+            const int32_t c0 = __ldg(a.child_ptr + p), c1 = __ldg(a.child_ptr + p + 1);
+            for (int32_t c = c0 + lg; c < c1; c += G) {
+                const int32_t j = __ldg(a.child + c);
+                if (j != i) r_value<DIM, QPOW>(xi, load_x<DIM>(a.x, j), cexp, C, -1.f);
+            }
+        }
+    }
+    // all lanes of the warp take part in the shuffles
+    rho = group_sum<G>(rho);
+    st = group_sum<G>(st);
+    A.x = group_sum<G>(A.x);
+    A.y = group_sum<G>(A.y);
+    C.x = group_sum<G>(C.x);
+    C.y = group_sum<G>(C.y);
+    if constexpr (DIM == 3) {
+        A.z = group_sum<G>(A.z);
+        C.z = group_sum<G>(C.z);
+    }
+    {
+        if (valid && lg == 0) {
+            float4 R = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int stride = DIM == 2 ? 2 : 4;
+            for (int p = 0; p < a.P; ++p) {
+                const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
+                R.x += v.x;
+                R.y += v.y;
+                R.z += v.z;
+            }
+            R.x -= C.x;
+            R.y -= C.y;
+            R.z -= C.z;
+            float4 xn;
+            xn.x = fmaf(a.alpha, R.x, A.x) / rho;
+            xn.y = fmaf(a.alpha, R.y, A.y) / rho;
+            xn.z = (DIM == 3) ? fmaf(a.alpha, R.z, A.z) / rho : 0.f;
+            xn.w = 0.f;
+            store_x<DIM>(a.x_out, i, xn);
+            const bool fin = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z);
+            if (!fin) atomicOr(a.flags, 1);
+            const double ex = (double)xn.x - xi.x, ey = (double)xn.y - xi.y, ez = (double)xn.z - xi.z;
+            v_dx2 = ex * ex + ey * ey + ez * ez;
+            v_x2 = (double)xi.x * xi.x + (double)xi.y * xi.y + (double)xi.z * xi.z;
+            v_st = (double)st;
+        }
+    }
+    // fixed-order block reduction of (dx2, x2, stress)
+    __shared__ double red[3][kGBlock / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v_dx2 += __shfl_xor_sync(0xffffffffu, v_dx2, o);
+        v_x2 += __shfl_xor_sync(0xffffffffu, v_x2, o);
+        v_st += __shfl_xor_sync(0xffffffffu, v_st, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = v_dx2;
+        red[1][threadIdx.x >> 5] = v_x2;
+        red[2][threadIdx.x >> 5] = v_st;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int w = 0; w < kGBlock / 32; ++w) s += red[threadIdx.x][w];
+        a.stat_partial[(int64_t)blockIdx.x * 3 + threadIdx.x] = s;
+    }
+}
+
+__global__ void k_stats_final(const double* __restrict__ partial, int nblocks, const int32_t* __restrict__ flags,
+                              mm_sweep_stats* __restrict__ out) {
+    __shared__ double red[3][32];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;  // 1 block of 1024 threads
+    double s[3] = {0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < nblocks; b += blockDim.x)
+        for (int k = 0; k < 3; ++k) s[k] += partial[(int64_t)b * 3 + k];
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(0xffffffffu, s[k], o);
+        if (lane == 0) red[k][wid] = s[k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t[3] = {0.0, 0.0, 0.0};
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            for (int k = 0; k < 3; ++k) t[k] += red[k][w];
+        out->dx2 = t[0];
+        out->x2 = t[1];
+        out->stress = 0.5 * t[2];
+        out->flags = *flags;
+        out->pad = 0;
+    }
+}
+
+// S part of mm_energy: per row, stress_i and sum_{j in S_i} of the same
+// per-pair transform as k_entropy_all (so the subtraction is consistent).
+template <int DIM, bool QPOW, int G>
+__global__ void __launch_bounds__(kGBlock) k_energy_s(int32_t n, const int64_t* __restrict__ rp,
+                                                      const int32_t* __restrict__ col, const float* __restrict__ d,
+                                                      const float* __restrict__ w, const float* __restrict__ x,
+                                                      float cq, double* __restrict__ partial,
+                                                      int32_t* __restrict__ coinc) {
+    const int lg = threadIdx.x & (G - 1);
+    const int64_t i = ((int64_t)blockIdx.x * kGBlock + threadIdx.x) / G;
+    float st = 0.f, ph = 0.f;
+    int32_t zc = 0;
+    if (i < n) {
+        const float4 xi = load_x<DIM>(x, i);
+        for (int64_t e = rp[i] + lg; e < rp[i + 1]; e += G) {
+            const float4 xj = load_x<DIM>(x, __ldg(col + e));
+            const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+            float r2 = fmaf(dx, dx, 0.f);
+            r2 = fmaf(dy, dy, r2);
+            if constexpr (DIM == 3) {
+                const float dz = xi.z - xj.z;
+                r2 = fmaf(dz, dz, r2);
+            }
+            zc += (r2 == 0.f) ? 1 : 0;
+            const float dist = sqrtf(r2);
+            const float dev = dist - __ldg(d + e);
+            st = fmaf(__ldg(w + e) * dev, dev, st);
+            const float l = lg2_approx(r2 + kEps2);
+            if constexpr (!QPOW) ph += l;
+            else ph += ex2_approx(fminf(cq * l, kExpClamp));
+        }
+    }
+    double a0 = st, a1 = ph;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        zc += __shfl_xor_sync(0xffffffffu, zc, o);
+    }
+    __shared__ double red[2][kGBlock / 32];
+    __shared__ int32_t redc[kGBlock / 32];
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = a0;
+        red[1][threadIdx.x >> 5] = a1;
+        redc[threadIdx.x >> 5] = zc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s0 = 0.0, s1 = 0.0;
+        int32_t c = 0;
+        for (int k = 0; k < kGBlock / 32; ++k) {
+            s0 += red[0][k];
+            s1 += red[1][k];
+            c += redc[k];
+        }
+        partial[(int64_t)blockIdx.x * 2] = s0;
+        partial[(int64_t)blockIdx.x * 2 + 1] = s1;
+        if (c) atomicAdd(coinc, c);
+    }
+}
+
+int pick_group(double mean_row) {
+    if (mean_row >= 32) return 32;
+    if (mean_row >= 16) return 16;
+    if (mean_row >= 8) return 8;
+    return 4;
+}
+
+}  // namespace
+
+int gather_blocks(int32_t n, double mean_row) {
+    const int G = pick_group(mean_row);
+    return (int)(((int64_t)n * G + kGBlock - 1) / kGBlock);
+}
+
+cudaError_t launch_gather(int dim, const GatherArgs& a, double mean_row, cudaStream_t st) {
+    const int G = pick_group(mean_row);
+    const int nb = gather_blocks(a.n, mean_row);
+    const float cexp = -(a.q + 2.0f) * 0.5f;
+    const bool qpow = a.q != 0.0f;
+    LaunchScope ls("gather_update", st);
+#define MM_G(D, Q)                                                                  \
+    switch (G) {                                                                    \
+        case 4: k_gather<D, Q, 4><<<nb, kGBlock, 0, st>>>(a, cexp); break;          \
+        case 8: k_gather<D, Q, 8><<<nb, kGBlock, 0, st>>>(a, cexp); break;          \
+        case 16: k_gather<D, Q, 16><<<nb, kGBlock, 0, st>>>(a, cexp); break;        \
+        default: k_gather<D, Q, 32><<<nb, kGBlock, 0, st>>>(a, cexp); break;        \
+    }
+    if (dim == 2) {
+        if (qpow) { MM_G(2, true) } else { MM_G(2, false) }
+    } else {
+        if (qpow) { MM_G(3, true) } else { MM_G(3, false) }
+    }
+#undef MM_G
+    return cudaGetLastError();
+}
+
+cudaError_t launch_stats_final(const double* partial, int nblocks, const int32_t* flags, mm_sweep_stats* out,
+                               cudaStream_t st) {
+    LaunchScope ls("stats_final", st);
+    k_stats_final<<<1, 1024, 0, st>>>(partial, nblocks, flags, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_energy_s(int dim, double q, int32_t n, const int64_t* rp, const int32_t* col, const float* d,
+                            const float* w, const float* x, double mean_row, double* partial, int32_t* coinc,
+                            cudaStream_t st) {
+    const int G = pick_group(mean_row);
+    const int nb = gather_blocks(n, mean_row);
+    const float cq = (float)(-q * 0.5);
+    const bool qpow = q != 0.0;
+    LaunchScope ls("energy_s", st);
+#define MM_E(D, Q)                                                                                  \
+    switch (G) {                                                                                    \
+        case 4: k_energy_s<D, Q, 4><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break;   \
+        case 8: k_energy_s<D, Q, 8><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break;   \
+        case 16: k_energy_s<D, Q, 16><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break; \
+        default: k_energy_s<D, Q, 32><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break; \
+    }
+    if (dim == 2) {
+        if (qpow) { MM_E(2, true) } else { MM_E(2, false) }
+    } else {
+        if (qpow) { MM_E(3, true) } else { MM_E(3, false) }
+    }
+#undef MM_E
+    return cudaGetLastError();
+}
+
+}  // namespace mm

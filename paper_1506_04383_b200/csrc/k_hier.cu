@@ -1,0 +1,423 @@
+// k_hier.cu — kernels (d): handshake heavy-edge matching, contraction,
+// coarse S^l, grouping maps into CSR, centroid/mass refresh, prolongation and
+// the coarsest-level initial layout.
+//
+// Contraction: "each block of the clustering is
+// contracted into a single node.  The weight of the node is set to the sum of
+// the weight of all nodes in the original block ... The weight of an edge
+// (u',v') is set to the sum of the weight of edges that run between block u'
+// and block v'."  The clustering is BASELINE.json's seeded heavy-edge
+// matching, read as Q16: synchronous handshake rounds; rating
+// omega_uv / (c_u c_v) compared exactly in int64; ties -> higher SplitMix64
+// hash of (seed, level, round, min, max) -> lower id; coarse id = rank of the
+// leader min(u, mate(u)).  All integer work, so the result is bit-identical to
+// the oracle's.
+//
+// Centroids (Q10-Q12): nu(v') = number of current-level
+// members, x'_v' = their unweighted mean; members are visited in ascending
+// id order from a CSR built by a stable sort, so the FP32 sum is deterministic.
+// Prolongation (Q15, BASELINE.json configs[2]): x_u = x_{P(u)} + 1e-3 (2U - 1)
+// per component, U from the counter RNG keyed (seed, JITTER, level, u*dim+k).
+#include <cub/cub.cuh>
+
+#include "k_hier.cuh"
+
+namespace mm {
+
+namespace {
+
+__device__ __forceinline__ uint64_t match_hash(uint64_t seed, int32_t level, int32_t round, int32_t u, int32_t v) {
+    const uint64_t lo = (uint64_t)(uint32_t)min(u, v), hi = (uint64_t)(uint32_t)max(u, v);
+    uint64_t k = mix64(seed ^ kTagMatch);
+    k = mix64(k ^ (uint64_t)level);
+    k = mix64(k ^ (uint64_t)round);
+    return mix64(k ^ ((lo << 32) | hi));
+}
+
+// One thread per vertex: pick the best unmatched neighbour.
+__global__ void k_match_pick(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                             const int32_t* __restrict__ omega, const int32_t* __restrict__ c,
+                             const int32_t* __restrict__ mate, int32_t* __restrict__ cand, uint64_t seed,
+                             int32_t level, int32_t round) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    if (mate[u] >= 0) {
+        cand[u] = -1;
+        return;
+    }
+    int32_t best = -1;
+    int64_t wb = 0, cb = 0;
+    uint64_t hb = 0;
+    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+        const int32_t v = col[e];
+        if (v == u || mate[v] >= 0) continue;
+        const int64_t wv = omega ? omega[e] : 1, cv = c[v];
+        const uint64_t hv = match_hash(seed, level, round, u, v);
+        bool better;
+        if (best < 0) {
+            better = true;
+        } else {
+            const int64_t lhs = wv * cb, rhs = wb * cv;  // wv/cv > wb/cb ?
+            if (lhs != rhs) better = lhs > rhs;
+            else if (hv != hb) better = hv > hb;
+            else better = v < best;
+        }
+        if (better) {
+            best = v;
+            wb = wv;
+            cb = cv;
+            hb = hv;
+        }
+    }
+    cand[u] = best;
+}
+
+__global__ void k_match_confirm(int32_t n, const int32_t* __restrict__ cand, int32_t* __restrict__ mate,
+                                int32_t* __restrict__ added) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    int32_t hit = 0;
+    if (u < n && mate[u] < 0) {
+        const int32_t v = cand[u];
+        if (v >= 0 && cand[v] == u) {
+            mate[u] = v;
+            hit = 1;
+        }
+    }
+    hit = __reduce_add_sync(0xffffffffu, hit);
+    if ((threadIdx.x & 31) == 0 && hit) atomicAdd(added, hit);
+}
+
+__global__ void k_leader_flag(int32_t n, const int32_t* __restrict__ mate, int32_t* __restrict__ flag) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int32_t m = mate[u];
+    flag[u] = (m < 0 || u < m) ? 1 : 0;
+}
+
+// cid = exclusive scan of flags; parent[u] = cid[leader(u)]; leader_of[p]; c'
+__global__ void k_parent(int32_t n, const int32_t* __restrict__ mate, const int32_t* __restrict__ cid,
+                         const int32_t* __restrict__ c, int32_t* __restrict__ parent, int32_t* __restrict__ c_next) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int32_t m = mate[u];
+    const int32_t lead = (m >= 0 && m < u) ? m : u;
+    const int32_t p = cid[lead];
+    parent[u] = p;
+    if (lead == u) c_next[p] = c[u] + (m >= 0 ? c[m] : 0);
+}
+
+// keys (parent[u] * nc + parent[v]) for crossing entries; intra-cluster -> sentinel nc*nc
+__global__ void k_edge_keys(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                            const int32_t* __restrict__ omega, const int32_t* __restrict__ parent, int64_t nc,
+                            uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int64_t pu = parent[u];
+    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+        const int64_t pv = parent[col[e]];
+        keys[e] = (pu != pv) ? (uint64_t)(pu * nc + pv) : (uint64_t)(nc * nc);
+        vals[e] = omega ? omega[e] : 1;
+    }
+}
+
+__global__ void k_run_heads(int64_t m, const uint64_t* __restrict__ keys, uint64_t sentinel, int32_t* __restrict__ head) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m) return;
+    const uint64_t k = keys[t];
+    head[t] = (k != sentinel && (t == 0 || keys[t - 1] != k)) ? 1 : 0;
+}
+
+// for each run head: write coarse col / omega (sum over the run) and count the row
+__global__ void k_run_emit(int64_t m, const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals,
+                           const int32_t* __restrict__ head, const int32_t* __restrict__ pos, int64_t nc,
+                           int32_t* __restrict__ ccol, int32_t* __restrict__ comega, int32_t* __restrict__ rowcnt) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= m || !head[t]) return;
+    const uint64_t k = keys[t];
+    int32_t s = 0;
+    for (int64_t r = t; r < m && keys[r] == k; ++r) s += vals[r];
+    const int32_t p = pos[t];
+    ccol[p] = (int32_t)(k % (uint64_t)nc);
+    comega[p] = s;
+    atomicAdd(rowcnt + (k / (uint64_t)nc), 1);
+}
+
+__global__ void k_i32_to_i64_rowptr(int32_t n, const int32_t* __restrict__ excl, int64_t total,
+                                    int64_t* __restrict__ rp) {
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) rp[t] = excl[t];
+    if (t == n) rp[n] = total;
+}
+
+__global__ void k_coarse_sset(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                              const int32_t* __restrict__ c, int dim, float* __restrict__ d, float* __restrict__ w) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const float su = dim == 2 ? sqrtf((float)c[u]) : cbrtf((float)c[u]);
+    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+        const int32_t v = col[e];
+        const float sv = dim == 2 ? sqrtf((float)c[v]) : cbrtf((float)c[v]);
+        const float dd = su + sv;
+        d[e] = dd;
+        w[e] = 1.0f / (dd * dd);
+    }
+}
+
+__global__ void k_iota(int32_t n, int32_t* __restrict__ a) {
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) a[t] = t;
+}
+
+__global__ void k_fill_i32(int64_t n, int32_t v, int32_t* __restrict__ a) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) a[t] = v;
+}
+
+__global__ void k_count(int32_t n, const int32_t* __restrict__ key, int32_t* __restrict__ cnt) {
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) atomicAdd(cnt + key[t], 1);
+}
+
+__global__ void k_compose(int32_t n, const int32_t* __restrict__ a, const int32_t* __restrict__ map,
+                          int32_t* __restrict__ out) {
+    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t < n) out[t] = map[a[t]];
+}
+
+template <int DIM>
+__global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
+                           const float* __restrict__ x, float4* __restrict__ reps) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= k) return;
+    const int32_t b = mptr[v], e = mptr[v + 1];
+    float sx = 0.f, sy = 0.f, sz = 0.f;
+    for (int32_t t = b; t < e; ++t) {
+        const float4 p = load_x<DIM>(x, mem[t]);
+        sx += p.x;
+        sy += p.y;
+        sz += p.z;
+    }
+    const float nu = (float)(e - b);
+    const float inv = 1.0f / nu;
+    reps[v] = make_float4(sx * inv, sy * inv, DIM == 3 ? sz * inv : 0.f, nu);
+}
+
+template <int DIM>
+__global__ void k_prolong(int32_t n, const int32_t* __restrict__ parent, const float* __restrict__ xc,
+                          uint64_t seed, int32_t level, float* __restrict__ x) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const float4 pc = load_x<DIM>(xc, parent[u]);
+    const uint64_t k0 = mix64(mix64(seed ^ kTagJitter) ^ (uint64_t)level);
+    float o[3];
+    const float pv[3] = {pc.x, pc.y, pc.z};
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        const float U = uniform24(mix64(k0 ^ ((uint64_t)u * DIM + c)));
+        o[c] = pv[c] + 1e-3f * (2.0f * U - 1.0f);
+    }
+    store_x<DIM>(x, u, make_float4(o[0], o[1], DIM == 3 ? o[2] : 0.f, 0.f));
+}
+
+template <int DIM>
+__global__ void k_init_box(int32_t n, const double* __restrict__ dsum, int64_t nnz, uint64_t seed, int32_t level,
+                           float* __restrict__ x) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const double dbar = nnz > 0 ? *dsum / (double)nnz : 1.0;
+    const float box = (float)(dbar * (DIM == 2 ? sqrt((double)n) : cbrt((double)n)));
+    const uint64_t k0 = mix64(mix64(seed ^ kTagInit) ^ (uint64_t)level);
+    float o[3];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) o[c] = box * uniform24(mix64(k0 ^ ((uint64_t)u * DIM + c)));
+    store_x<DIM>(x, u, make_float4(o[0], o[1], DIM == 3 ? o[2] : 0.f, 0.f));
+}
+
+// FP64 sum of a float array (one block, fixed order)
+__global__ void k_sum_f32(int64_t m, const float* __restrict__ a, double* __restrict__ out) {
+    __shared__ double red[32];
+    double s = 0.0;
+    for (int64_t t = threadIdx.x; t < m; t += blockDim.x) s += (double)a[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+        *out = t;
+    }
+}
+
+inline int nblk(int64_t n, int b = 256) { return (int)((n + b - 1) / b); }
+
+}  // namespace
+
+// ------------------------------------------------------------------ host side
+
+cudaError_t run_match_round(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* omega,
+                            const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
+                            int32_t round, int32_t* added, cudaStream_t st) {
+    {
+        LaunchScope ls("match_pick", st);
+        k_match_pick<<<nblk(n), 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round);
+    }
+    {
+        LaunchScope ls("match_confirm", st);
+        k_match_confirm<<<nblk(n), 256, 0, st>>>(n, cand, mate, added);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fill(int64_t n, int32_t v, int32_t* a, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    LaunchScope ls("fill", st);
+    k_fill_i32<<<nblk(n), 256, 0, st>>>(n, v, a);
+    return cudaGetLastError();
+}
+
+size_t scan_temp_bytes(int32_t n) {
+    size_t b = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, n);
+    return b;
+}
+
+size_t sort_temp_bytes_u64(int64_t m) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, m);
+    return b;
+}
+
+size_t sort_temp_bytes_i32(int32_t n) {
+    size_t b = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
+                                    (int32_t*)nullptr, n);
+    return b;
+}
+
+cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, void* tmp, size_t tmp_bytes,
+                               cudaStream_t st) {
+    LaunchScope ls("cub_scan", st);
+    return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n, st);
+}
+
+cudaError_t contract_leaders(int32_t n, const int32_t* mate, const int32_t* c, int32_t* flag, int32_t* cid,
+                             int32_t* parent, int32_t* c_next, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+    {
+        LaunchScope ls("leader_flag", st);
+        k_leader_flag<<<nblk(n), 256, 0, st>>>(n, mate, flag);
+    }
+    cudaError_t e = exclusive_scan_i32(flag, cid, n, tmp, tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    LaunchScope ls("parent", st);
+    k_parent<<<nblk(n), 256, 0, st>>>(n, mate, cid, c, parent, c_next);
+    return cudaGetLastError();
+}
+
+cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
+                           const int32_t* parent, int32_t nc, uint64_t* keys, uint64_t* keys_alt, int32_t* vals,
+                           int32_t* vals_alt, int32_t* head, int32_t* pos, int32_t* ccol_tmp,
+                           int32_t* comega_tmp, int32_t* rowcnt, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+    cudaError_t e;
+    {
+        LaunchScope ls("edge_keys", st);
+        k_edge_keys<<<nblk(n), 256, 0, st>>>(n, rp, col, omega, parent, nc, keys, vals);
+    }
+    const uint64_t sentinel = (uint64_t)nc * (uint64_t)nc;
+    int end_bit = 1;
+    while (end_bit < 64 && (sentinel >> end_bit) != 0) ++end_bit;
+    {
+        LaunchScope ls("cub_sort_edges", st);
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_alt, vals, vals_alt, nnz, 0, end_bit, st);
+        if (e != cudaSuccess) return e;
+    }
+    {
+        LaunchScope ls("run_heads", st);
+        k_run_heads<<<nblk(nnz), 256, 0, st>>>(nnz, keys_alt, sentinel, head);
+    }
+    e = exclusive_scan_i32(head, pos, (int32_t)nnz, tmp, tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    e = launch_fill(nc + 1, 0, rowcnt, st);
+    if (e != cudaSuccess) return e;
+    LaunchScope ls("run_emit", st);
+    k_run_emit<<<nblk(nnz), 256, 0, st>>>(nnz, keys_alt, vals_alt, head, pos, nc, ccol_tmp, comega_tmp, rowcnt);
+    return cudaGetLastError();
+}
+
+cudaError_t rowptr_from_counts(int32_t nc, const int32_t* rowcnt, int32_t* excl, int64_t total, int64_t* rp,
+                               void* tmp, size_t tmp_bytes, cudaStream_t st) {
+    cudaError_t e = exclusive_scan_i32(rowcnt, excl, nc, tmp, tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    LaunchScope ls("rowptr", st);
+    k_i32_to_i64_rowptr<<<nblk(nc + 1), 256, 0, st>>>(nc, excl, total, rp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_coarse_sset(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* c, int dim,
+                               float* d, float* w, cudaStream_t st) {
+    LaunchScope ls("coarse_sset", st);
+    k_coarse_sset<<<nblk(n), 256, 0, st>>>(n, rp, col, c, dim, d, w);
+    return cudaGetLastError();
+}
+
+cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr, int32_t* members,
+                         int32_t* key_sorted, int32_t* iota, int32_t* cnt, void* tmp, size_t tmp_bytes,
+                         cudaStream_t st) {
+    cudaError_t e;
+    {
+        LaunchScope ls("iota", st);
+        k_iota<<<nblk(n), 256, 0, st>>>(n, iota);
+    }
+    int end_bit = 1;
+    while (end_bit < 31 && ((k - 1) >> end_bit) != 0) ++end_bit;
+    {
+        LaunchScope ls("cub_sort_group", st);
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_sorted, iota, members, n, 0, end_bit, st);
+        if (e != cudaSuccess) return e;
+    }
+    e = launch_fill(k + 1, 0, cnt, st);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope ls("count", st);
+        k_count<<<nblk(n), 256, 0, st>>>(n, key, cnt);
+    }
+    // exclusive scan over k+1 entries: ptr[k] = n
+    return exclusive_scan_i32(cnt, ptr, k + 1, tmp, tmp_bytes, st);
+}
+
+cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int32_t* out, cudaStream_t st) {
+    LaunchScope ls("compose", st);
+    k_compose<<<nblk(n), 256, 0, st>>>(n, a, map, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_centroid(int dim, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
+                            float4* reps, cudaStream_t st) {
+    LaunchScope ls("centroid", st);
+    if (dim == 2) k_centroid<2><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, reps);
+    else k_centroid<3><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, reps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
+                           int32_t level, float* x, cudaStream_t st) {
+    LaunchScope ls("prolong", st);
+    if (dim == 2) k_prolong<2><<<nblk(n), 256, 0, st>>>(n, parent, xc, seed, level, x);
+    else k_prolong<3><<<nblk(n), 256, 0, st>>>(n, parent, xc, seed, level, x);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,
+                            int32_t level, float* x, cudaStream_t st) {
+    {
+        LaunchScope ls("sum_d", st);
+        k_sum_f32<<<1, 1024, 0, st>>>(nnz, d, dsum);
+    }
+    LaunchScope ls("init_box", st);
+    if (dim == 2) k_init_box<2><<<nblk(n), 256, 0, st>>>(n, dsum, nnz, seed, level, x);
+    else k_init_box<3><<<nblk(n), 256, 0, st>>>(n, dsum, nnz, seed, level, x);
+    return cudaGetLastError();
+}
+
+}  // namespace mm

@@ -1,0 +1,37 @@
+// k_hier.cuh — host launchers of the hierarchy / centroid / prolongation kernels.
+#pragma once
+#include "mm_common.cuh"
+
+namespace mm {
+
+cudaError_t run_match_round(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* omega,
+                            const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
+                            int32_t round, int32_t* added, cudaStream_t st);
+cudaError_t launch_fill(int64_t n, int32_t v, int32_t* a, cudaStream_t st);
+size_t scan_temp_bytes(int32_t n);
+size_t sort_temp_bytes_u64(int64_t m);
+size_t sort_temp_bytes_i32(int32_t n);
+cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, void* tmp, size_t tmp_bytes,
+                               cudaStream_t st);
+cudaError_t contract_leaders(int32_t n, const int32_t* mate, const int32_t* c, int32_t* flag, int32_t* cid,
+                             int32_t* parent, int32_t* c_next, void* tmp, size_t tmp_bytes, cudaStream_t st);
+cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
+                           const int32_t* parent, int32_t nc, uint64_t* keys, uint64_t* keys_alt, int32_t* vals,
+                           int32_t* vals_alt, int32_t* head, int32_t* pos, int32_t* ccol_tmp,
+                           int32_t* comega_tmp, int32_t* rowcnt, void* tmp, size_t tmp_bytes, cudaStream_t st);
+cudaError_t rowptr_from_counts(int32_t nc, const int32_t* rowcnt, int32_t* excl, int64_t total, int64_t* rp,
+                               void* tmp, size_t tmp_bytes, cudaStream_t st);
+cudaError_t launch_coarse_sset(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* c, int dim,
+                               float* d, float* w, cudaStream_t st);
+cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr, int32_t* members,
+                         int32_t* key_sorted, int32_t* iota, int32_t* cnt, void* tmp, size_t tmp_bytes,
+                         cudaStream_t st);
+cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int32_t* out, cudaStream_t st);
+cudaError_t launch_centroid(int dim, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
+                            float4* reps, cudaStream_t st);
+cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
+                           int32_t level, float* x, cudaStream_t st);
+cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,
+                            int32_t level, float* x, cudaStream_t st);
+
+}  // namespace mm

@@ -1,0 +1,110 @@
+"""-m gpu: mm_energy parity and full-run mm_layout parity (final energy within
+1e-3 relative, BASELINE.json north_star), at oracle-sized scales of every
+config's generator, plus the coarsest-level / prolongation pieces."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import helpers as H
+from tests.gpu_common import ENERGY_TOL, workload
+from workloads import configs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import torch
+
+    import paper_1506_04383_b200 as mm
+
+    assert torch.cuda.is_available()
+    mm.load()
+    return mm
+
+
+def _rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+@pytest.mark.parametrize("name,dim,q", [("cfg1", 2, 0.0), ("cfg2_rgg8192", 2, 0.0), ("cfg5_grid12", 3, 0.8),
+                                        ("cfg4_cl20000", 2, 0.0)])
+def test_energy_parity(mm, name, dim, q):
+    w = workload(name)
+    x = w.x0 if w.x0 is not None else configs.random_state(w.n, dim, seed=4, scale=w.n ** (1 / dim))
+    S = mm.sset_to_device(w.S)
+    e = mm.energy(S, mm.coords_to_device(x), w.alpha, q)
+    o = oracle.energy(w.S, x.astype(np.float64), w.alpha, q)
+    assert _rel(e[0], o[0]) <= 1e-5, (e, o)
+    assert _rel(e[1], o[1]) <= 1e-4, (e, o)
+    assert _rel(e[2], o[2]) <= ENERGY_TOL * 0.1, (e, o)
+
+
+def test_energy_worked_example(mm):
+    """golden/path3_energy.txt through the GPU."""
+    gold = H.read_golden("path3_energy.txt")[0]
+    g = H.path(3)
+    S = H.sset_with(g, np.ones(4))
+    x = np.array([[0.0, 0.0], [1.0, 0.0], [2.0, 0.0]], dtype=np.float32)
+    e = mm.energy(mm.sset_to_device(S), mm.coords_to_device(x), 0.008, 0.0)
+    np.testing.assert_allclose(e, gold, rtol=1e-5, atol=1e-7)
+
+
+def test_energy_coincident_error(mm):
+    g = H.path(3)
+    S = H.sset_with(g, np.ones(4))
+    x = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 0.0]], dtype=np.float32)
+    with pytest.raises(mm.MMError) as ei:
+        mm.energy(mm.sset_to_device(S), mm.coords_to_device(x), 0.1, 0.0)
+    assert ei.value.status == -3
+
+
+def test_layout_exact_cfg1_full_run(mm):
+    """configs[0] exactly as specified: 50 exact sweeps from the seeded start."""
+    w = workload("cfg1")
+    S = mm.sset_to_device(w.S)
+    x, rep = mm.layout(None, S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=mm.coords_to_device(w.x0))
+    xo, eo, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=w.x0.astype(np.float64))
+    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep, eo)
+    # isolate kernel error from trajectory divergence: oracle energy of the GPU layout
+    eg = oracle.energy(w.S, mm.coords_from_device(x, 2), w.alpha, w.q)
+    assert _rel(rep["energy"], eg[2]) <= 1e-4
+    assert rep["vertex_updates"] == w.n * w.sweeps
+
+
+def test_layout_exact_rgg_full_run(mm):
+    w = workload("cfg2_rgg4096")
+    S = mm.sset_to_device(w.S)
+    x, rep = mm.layout(None, S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=mm.coords_to_device(w.x0))
+    xo, eo, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=w.x0.astype(np.float64))
+    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep, eo)
+
+
+@pytest.mark.parametrize("name,n_stop", [("cfg3_mesh64", 200), ("cfg5_grid16", 200), ("cfg4_cl20000", 1000),
+                                         ("cfg3_mesh128", 1000)])
+def test_layout_multilevel_full_run(mm, name, n_stop):
+    """Multilevel runs (h = 2, per-level sweeps of the config) on scaled-down
+    instances of configs[2..4]'s generators."""
+    w = workload(name)
+    g = mm.graph_to_device(w.graph)
+    S = mm.sset_to_device(w.S)
+    x, rep = mm.layout(g, S, w.dim, w.alpha, w.q, w.h, [w.sweeps], w.seed, n_stop=n_stop)
+    xo, eo, nl = oracle.layout(w.graph, w.S, w.dim, w.alpha, w.q, w.h, [w.sweeps], w.seed, n_stop=n_stop)
+    assert rep["levels"] == nl
+    eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), w.alpha, w.q)
+    assert _rel(rep["energy"], eg[2]) <= 1e-4, (rep["energy"], eg)
+    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (name, rep["energy"], eo)
+
+
+def test_layout_in_place(mm):
+    """x_init == x_out is allowed (the library iterates from a copy)."""
+    w = workload("cfg1_grid16")
+    S = mm.sset_to_device(w.S)
+    xd = mm.coords_to_device(w.x0)
+    x2, rep = mm.layout(None, S, 2, w.alpha, w.q, 0, [3], w.seed, x_init=xd, out=xd)
+    xo, eo, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [3], w.seed, x_init=w.x0.astype(np.float64))
+    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL

@@ -1,0 +1,204 @@
+"""-m gpu: one-sweep parity of mm_sweep (Eq.(2) exact and Eq.(3) approximate)
+against the FP64 oracle, through the C-ABI, plus closed forms, determinism
+and edge cases."""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from tests import helpers as H
+from tests.gpu_common import assert_sweep_parity, oracle_hierarchy, sample_rows, workload
+from workloads import configs, graphs, sset
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mm():
+    import torch
+
+    import paper_1506_04383_b200 as mm
+
+    assert torch.cuda.is_available()
+    mm.load()
+    return mm
+
+
+def _gpu_sweep(mm, S, x, alpha, q, parent=None, anc=None, k=0, stats=False):
+    import torch
+
+    Sd = mm.sset_to_device(S)
+    xd = mm.coords_to_device(x)
+    kw = {}
+    if parent is not None:
+        kw = dict(parent=torch.from_numpy(np.ascontiguousarray(parent, np.int32)).cuda(),
+                  ancestor=torch.from_numpy(np.ascontiguousarray(anc, np.int32)).cuda(), k=k)
+    r = mm.sweep(Sd, xd, alpha, q, stats=stats, **kw)
+    torch.cuda.synchronize()
+    if stats:
+        y, st = r
+        return mm.coords_from_device(y, x.shape[1]), st
+    return mm.coords_from_device(r, x.shape[1])
+
+
+# ------------------------------------------------------------------ exact, all rows
+@pytest.mark.parametrize("name", ["cfg1", "cfg1_grid33", "cfg2_rgg4096", "cfg2_rgg8192"])
+def test_exact_sweep_all_rows(mm, name):
+    w = workload(name)
+    x = w.x0.astype(np.float64)
+    got = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q)
+    want = oracle.sweep_exact(w.S, x, w.alpha, w.q)
+    assert_sweep_parity(got, want, name)
+
+
+@pytest.mark.parametrize("n,dim,q", [(1, 2, 0.0), (2, 2, 0.0), (3, 3, 0.8), (255, 2, 0.0), (257, 2, 0.8),
+                                     (1023, 3, 0.0), (1025, 3, 0.8), (4097, 2, 0.5)])
+def test_exact_sweep_ragged_sizes(mm, n, dim, q):
+    """Sizes around the 256-target tile and 1024-target CTA boundaries."""
+    if n == 1:
+        g = graphs.Graph(np.zeros(2, np.int64), np.zeros(0, np.int32))
+        pytest.skip("n = 1 has an empty S row: rho = 0 is invalid input (Q22)")
+    g = H.random_connected(n, n // 2 + 1, seed=n)
+    S = sset.hop2_sset(g) if n > 3 else H.sset_with(g, np.ones(g.nnz))
+    x = configs.random_state(n, dim, seed=n + 1, scale=math.sqrt(n))
+    got = _gpu_sweep(mm, S, x, 0.05, q)
+    want = oracle.sweep_exact(S, x.astype(np.float64), 0.05, q)
+    assert_sweep_parity(got, want, f"n={n} dim={dim} q={q}")
+
+
+def test_exact_sweep_cfg2_full_sampled_rows(mm):
+    """configs[1] at full size (n = 65,428 LCC), launch configuration of bench.py,
+    oracle evaluated on 2,048 sampled rows (plus the max-|S_i| rows)."""
+    w = workload("cfg2")
+    got = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q)
+    rl = w.S.row_lengths()
+    rows = sample_rows(w.n, 2048, seed=5, extra=np.argsort(rl)[-8:])
+    want = oracle.sweep_exact(w.S, w.x0.astype(np.float64), w.alpha, w.q, rows=rows)
+    assert_sweep_parity(got[rows], want, "cfg2 sampled")
+
+
+def test_exact_sweep_3d_q08(mm):
+    w = workload("cfg5_grid12")
+    x = configs.random_state(w.n, 3, seed=3, scale=12.0)
+    got = _gpu_sweep(mm, w.S, x, w.alpha, w.q)
+    want = oracle.sweep_exact(w.S, x.astype(np.float64), w.alpha, w.q)
+    assert_sweep_parity(got, want, "grid12^3 q=0.8")
+
+
+# ------------------------------------------------------------------ closed form at scale
+@pytest.mark.parametrize("n,q", [(65536, 0.0), (4099, 0.8)])
+def test_ring_closed_form(mm, n, q):
+    """one sweep of a regular n-gon (S = ring edges) gives the n-gon of
+    radius R' = R cos(2pi/n) + d sin(pi/n) + (alpha/2) sum_k R c_k/(2R^2 c_k)^(1+q/2);
+    exercises the full O(n^2) kernel against an FP64 formula (no oracle)."""
+    R, alpha, d = 0.5 * n / math.pi, 0.05, 1.0
+    th = 2 * np.pi * np.arange(n) / n
+    x = (R * np.stack([np.cos(th), np.sin(th)], axis=1)).astype(np.float32)
+    g = H.cycle(n)
+    S = H.sset_with(g, np.full(g.nnz, d))
+    got = _gpu_sweep(mm, S, x, alpha, q)
+    k = np.arange(2, n - 1)
+    ck = 1 - np.cos(2 * np.pi * k / n)
+    ent = alpha * (n - 3) / (4 * R) if q == 0 else 0.5 * alpha * np.sum(R * ck / (2 * R * R * ck) ** (1 + q / 2))
+    xr = x.astype(np.float64)
+    Rin = np.linalg.norm(xr, axis=1)  # exact radius of the FP32 input points
+    Rp = Rin * math.cos(2 * math.pi / n) + d * math.sin(math.pi / n) + ent
+    want = (Rp / Rin)[:, None] * xr
+    assert_sweep_parity(got, want, f"ring n={n}")
+
+
+# ------------------------------------------------------------------ Eq.(3)
+@pytest.mark.parametrize("name,h", [("cfg3_mesh64", 2), ("cfg3_mesh64", 1), ("cfg5_grid16", 2),
+                                    ("cfg4_cl20000", 2), ("cfg3_mesh128", 3)])
+def test_approx_sweep_all_rows(mm, name, h):
+    w = workload(name)
+    lv = oracle_hierarchy(name)
+    L = len(lv) - 1
+    hp = min(h, L)
+    anc = oracle.ancestor(lv, 0, hp)
+    k = lv[hp].n
+    x = configs.random_state(w.n, w.dim, seed=11, scale=math.sqrt(w.n))
+    got = _gpu_sweep(mm, w.S, x, w.alpha, w.q, lv[0].parent, anc, k)
+    want = oracle.sweep_approx(w.S, x.astype(np.float64), w.alpha, w.q, lv[0].parent, anc, k)
+    assert_sweep_parity(got, want, f"{name} h={h}")
+
+
+@pytest.mark.parametrize("name,rows", [("cfg3", 4096), ("cfg4", 2048), ("cfg5", 1024)])
+def test_approx_sweep_full_size_sampled(mm, name, rows):
+    """Full-size configs[2..4]: the GPU sweeps every vertex; the oracle
+    evaluates sampled rows with its own hierarchy (maps are bit-identical,
+    test_gpu_hierarchy)."""
+    w = workload(name)
+    lv = oracle_hierarchy(name)
+    anc = oracle.ancestor(lv, 0, 2)
+    k = lv[2].n
+    x = configs.random_state(w.n, w.dim, seed=12, scale=w.n ** (1.0 / w.dim))
+    got = _gpu_sweep(mm, w.S, x, w.alpha, w.q, lv[0].parent, anc, k)
+    rl = w.S.row_lengths()
+    r = sample_rows(w.n, rows, seed=13, extra=np.argsort(rl)[-4:])
+    want = oracle.sweep_approx(w.S, x.astype(np.float64), w.alpha, w.q, lv[0].parent, anc, k, rows=r)
+    assert_sweep_parity(got[r], want, f"{name} sampled")
+
+
+def test_approx_identity_map_equals_exact(mm):
+    """P:281 on the GPU: M = identity makes Eq.(3) equal Eq.(2)."""
+    w = workload("cfg2_rgg4096")
+    ident = np.arange(w.n, dtype=np.int32)
+    a = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q, ident, ident, w.n)
+    b = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q)
+    assert_sweep_parity(a, b.astype(np.float64), "identity vs exact")
+
+
+def test_approx_single_cluster_equals_exact(mm):
+    w = workload("cfg1")
+    zero = np.zeros(w.n, dtype=np.int32)
+    a = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q, zero, zero, 1)
+    want = oracle.sweep_exact(w.S, w.x0.astype(np.float64), w.alpha, w.q)
+    assert_sweep_parity(a, want, "single cluster")
+
+
+# ------------------------------------------------------------------ properties
+def test_determinism_bitwise(mm):
+    w = workload("cfg2_rgg8192")
+    a = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q)
+    b = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q)
+    assert np.array_equal(a, b)
+    w3 = workload("cfg3_mesh64")
+    lv = oracle_hierarchy("cfg3_mesh64")
+    anc = oracle.ancestor(lv, 0, 2)
+    x = configs.random_state(w3.n, 2, seed=1, scale=64.0)
+    c = _gpu_sweep(mm, w3.S, x, w3.alpha, w3.q, lv[0].parent, anc, lv[2].n)
+    d = _gpu_sweep(mm, w3.S, x, w3.alpha, w3.q, lv[0].parent, anc, lv[2].n)
+    assert np.array_equal(c, d)
+
+
+def test_translation_invariance_gpu(mm):
+    w = workload("cfg1")
+    a = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q)
+    t = np.array([3.0, -2.0], dtype=np.float32)
+    b = _gpu_sweep(mm, w.S, w.x0 + t, w.alpha, w.q)
+    assert_sweep_parity(b - t, a.astype(np.float64), "translation")
+
+
+def test_sweep_stats(mm):
+    """Relative change and stress from the fused reduction (e)."""
+    w = workload("cfg2_rgg4096")
+    got, st = _gpu_sweep(mm, w.S, w.x0, w.alpha, w.q, stats=True)
+    x = w.x0.astype(np.float64)
+    want = oracle.sweep_exact(w.S, x, w.alpha, w.q)
+    rc = oracle.relative_change(x, want)
+    assert st["flags"] == 0
+    assert abs(math.sqrt(st["dx2"] / st["x2"]) - rc) <= 1e-4 * rc
+    stress = oracle.energy(w.S, x, 0.0, 0.0)[0]
+    assert abs(st["stress"] - stress) <= 1e-4 * stress
+
+
+def test_nonfinite_flag(mm):
+    w = workload("cfg1")
+    x = w.x0.copy()
+    x[5, 0] = np.nan
+    _, st = _gpu_sweep(mm, w.S, x, w.alpha, w.q, stats=True)
+    assert st["flags"] & 1
