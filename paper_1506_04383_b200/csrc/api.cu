@@ -162,7 +162,8 @@ struct SweepBufs {
     float* part = nullptr;
     double* stat_partial = nullptr;
     int32_t* flags = nullptr;
-    float4* reps = nullptr;
+    float4* rep_hi = nullptr;
+    float4* rep_lo = nullptr;
     int32_t* mptr = nullptr;
     int32_t* mem = nullptr;
     int32_t* cptr = nullptr;
@@ -180,13 +181,15 @@ size_t cub_tmp_bytes(int32_t n) {
 
 size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) {
     const int32_t n_src = approx ? k : n;
-    RepulsePlan p = plan_repulse(n, n_src, dim);
-    size_t b = al((size_t)p.P * n * stride_of(dim) * sizeof(float));
+    RepulsePlan p = plan_repulse(n, n_src, dim, approx, true);
+    RepulsePlan p2 = plan_repulse(n, n_src, dim, approx, false);
+    const int slots = std::max(p.slots, p2.slots);
+    size_t b = al((size_t)slots * n * stride_of(dim) * sizeof(float));
     (void)mean_row;
     b += al((size_t)gather_blocks(n, 1e9) * 3 * sizeof(double));  // bound: G = 32
     b += al(sizeof(int32_t) * 4);
     if (approx) {
-        b += al((size_t)k * sizeof(float4)) + al((size_t)(k + 1) * 4) + al((size_t)n * 4);
+        b += 2 * al((size_t)k * sizeof(float4)) + al((size_t)(k + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)(n + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)n * 4) * 2 + al((size_t)(std::max(n, k) + 2) * 4);
         b += al(cub_tmp_bytes(n));
@@ -196,13 +199,15 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
 
 bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double mean_row, SweepBufs& sb) {
     const int32_t n_src = approx ? k : n;
-    RepulsePlan p = plan_repulse(n, n_src, dim);
-    sb.part = cv.take<float>((size_t)p.P * n * stride_of(dim));
+    RepulsePlan p = plan_repulse(n, n_src, dim, approx, true);
+    RepulsePlan p2 = plan_repulse(n, n_src, dim, approx, false);
+    sb.part = cv.take<float>((size_t)std::max(p.slots, p2.slots) * n * stride_of(dim));
     (void)mean_row;
     sb.stat_partial = cv.take<double>((size_t)gather_blocks(n, 1e9) * 3);
     sb.flags = cv.take<int32_t>(4);
     if (approx) {
-        sb.reps = cv.take<float4>(k);
+        sb.rep_hi = cv.take<float4>(k);
+        sb.rep_lo = cv.take<float4>(k);
         sb.mptr = cv.take<int32_t>(k + 1);
         sb.mem = cv.take<int32_t>(n);
         sb.cptr = cv.take<int32_t>(n + 1);
@@ -234,13 +239,13 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     cudaError_t e;
     RepulsePlan p;
     if (ap) {
-        e = launch_centroid(dim, ap->k, sb.mptr, sb.mem, x_in, sb.reps, st);
+        e = launch_centroid(dim, ap->k, sb.mptr, sb.mem, x_in, sb.rep_hi, sb.rep_lo, st);
         if (e != cudaSuccess) return e;
-        p = plan_repulse(n, ap->k, dim);
-        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.reps, ap->ancestor, p, sb.part, st);
+        p = plan_repulse(n, ap->k, dim, true, qpow);
+        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, ap->ancestor, p, sb.part, st);
     } else {
-        p = plan_repulse(n, n, dim);
-        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, p, sb.part, st);
+        p = plan_repulse(n, n, dim, false, qpow);
+        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, nullptr, p, sb.part, st);
     }
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(sb.flags, 0, sizeof(int32_t), st);
@@ -255,7 +260,8 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     ga.alpha = alpha;
     ga.q = q;
     ga.part = sb.part;
-    ga.P = p.P;
+    ga.sch = p.sch;
+    ga.tpb = repulse_targets_per_block(dim);
     ga.parent = ap ? ap->parent : nullptr;
     ga.child_ptr = ap ? sb.cptr : nullptr;
     ga.child = ap ? sb.child : nullptr;

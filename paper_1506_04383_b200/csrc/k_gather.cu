@@ -116,7 +116,11 @@ __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
         if (valid && lg == 0) {
             float4 R = make_float4(0.f, 0.f, 0.f, 0.f);
             const int stride = DIM == 2 ? 2 : 4;
-            for (int p = 0; p < a.P; ++p) {
+            // partial slots written for this vertex's target block (static schedule)
+            const int64_t tb = i / a.tpb;
+            const int32_t nslot = sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
+                                  sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
+            for (int p = 0; p < nslot; ++p) {
                 const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
                 R.x += v.x;
                 R.y += v.y;

@@ -184,22 +184,27 @@ __global__ void k_compose(int32_t n, const int32_t* __restrict__ a, const int32_
     if (t < n) out[t] = map[a[t]];
 }
 
+// Representative x'_v' = unweighted mean of the members (Q11),
+// accumulated in FP64 in ascending member order and stored as hi + lo floats
+// (hi = fl32(mean), lo = fl32(mean - hi)); rep_hi.w = nu(v') (Q10).
 template <int DIM>
 __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
-                           const float* __restrict__ x, float4* __restrict__ reps) {
+                           const float* __restrict__ x, float4* __restrict__ rep_hi, float4* __restrict__ rep_lo) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= k) return;
     const int32_t b = mptr[v], e = mptr[v + 1];
-    float sx = 0.f, sy = 0.f, sz = 0.f;
+    double sx = 0.0, sy = 0.0, sz = 0.0;
     for (int32_t t = b; t < e; ++t) {
         const float4 p = load_x<DIM>(x, mem[t]);
         sx += p.x;
         sy += p.y;
         sz += p.z;
     }
-    const float nu = (float)(e - b);
-    const float inv = 1.0f / nu;
-    reps[v] = make_float4(sx * inv, sy * inv, DIM == 3 ? sz * inv : 0.f, nu);
+    const double nu = (double)(e - b);
+    const double mx = sx / nu, my = sy / nu, mz = DIM == 3 ? sz / nu : 0.0;
+    const float hx = (float)mx, hy = (float)my, hz = (float)mz;
+    rep_hi[v] = make_float4(hx, hy, hz, (float)nu);
+    rep_lo[v] = make_float4((float)(mx - hx), (float)(my - hy), (float)(mz - hz), 0.f);
 }
 
 template <int DIM>
@@ -393,10 +398,10 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
 }
 
 cudaError_t launch_centroid(int dim, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                            float4* reps, cudaStream_t st) {
+                            float4* rep_hi, float4* rep_lo, cudaStream_t st) {
     LaunchScope ls("centroid", st);
-    if (dim == 2) k_centroid<2><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, reps);
-    else k_centroid<3><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, reps);
+    if (dim == 2) k_centroid<2><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo);
+    else k_centroid<3><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo);
     return cudaGetLastError();
 }
 

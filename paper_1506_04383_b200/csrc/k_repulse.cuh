@@ -6,10 +6,23 @@
 
 namespace mm {
 
+// Static persistent schedule of the all-pairs kernels: the (target block,
+// source tile) space of U = TB * Ub work units is split into G contiguous
+// ranges [g*U/G, (g+1)*U/G).  Requires G <= U (every range non-empty).
+struct Sched {
+    int64_t U = 1;
+    int32_t Ub = 1;   // source tiles per target block
+    int32_t TB = 1;   // target blocks
+    int32_t G = 1;    // CTAs
+};
+// first CTA whose range contains work unit a: max{g : floor(g U / G) <= a}
+__host__ __device__ __forceinline__ int32_t sched_first_cta(int64_t a, const Sched& s) {
+    return (int32_t)(((a + 1) * (int64_t)s.G - 1) / s.U);
+}
+
 struct RepulsePlan {
-    int tblocks = 1;   // CTAs along targets
-    int P = 1;         // source chunks (grid.y) = number of partial-sum slices
-    int32_t chunk = 0; // sources per chunk
+    Sched sch;
+    int slots = 1;     // max partial slots per target (size of the partial buffer / n)
 };
 struct EntropyPlan {
     int tblocks = 1;
@@ -17,10 +30,11 @@ struct EntropyPlan {
     int32_t chunk = 0;
 };
 
-RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim);
+RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, bool qpow);
+int repulse_targets_per_block(int dim);
 cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_tgt, const float* x,
-                           int32_t n_src, const float4* reps, const int32_t* anc, const RepulsePlan& p,
-                           float* part, cudaStream_t st);
+                           int32_t n_src, const float4* rep_hi, const float4* rep_lo, const int32_t* anc,
+                           const RepulsePlan& p, float* part, cudaStream_t st);
 EntropyPlan plan_entropy(int32_t n);
 cudaError_t launch_entropy_all(int dim, double q, int32_t n, const float* x, const EntropyPlan& p,
                                double* partial, int32_t* coinc, cudaStream_t st);
@@ -35,8 +49,9 @@ struct GatherArgs {
     const float* x;
     float alpha;
     float q;
-    const float* part;   // [P][n] stride 2 (dim 2) or 4 (dim 3)
-    int P;
+    const float* part;   // [slots][n] stride 2 (dim 2) or 4 (dim 3)
+    Sched sch;           // schedule that produced `part` (slot count per target block)
+    int tpb;             // targets per block of that schedule
     // Eq.(3) sibling term (nullable: exact mode)
     const int32_t* parent;
     const int32_t* child_ptr;

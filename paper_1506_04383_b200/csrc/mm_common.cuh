@@ -31,10 +31,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
     return y;
 }
 
-// Softening added to r^2 before the reciprocal (reading Q6): 1e-36 is a
-// normal float, so an exactly coincident pair gives 0 * rcp(1e-36) = 0 and
-// any pair with r > ~4e-15 is unaffected after rounding.
-constexpr float kEps2 = 1e-36f;
+// Softening added to r^2 before the reciprocal (reading Q6): an exactly
+// coincident pair gives 0 * rcp(eps) = 0.  1e-18 keeps the product of two
+// softened r^2 (batched reciprocal, k_repulse.cu) a normal float; it changes
+// r^2 by < 1e-6 relative for every pair with r > 1e-6.
+constexpr float kEps2 = 1e-18f;
 // Clamp of the exponent for q > 0 so that ex2 stays finite for coincident
 // (masked) pairs: 2^126 < FLT_MAX.
 constexpr float kExpClamp = 126.0f;
@@ -48,6 +49,40 @@ __device__ __forceinline__ float inv_pow(float r2, float c) {
     } else {
         return ex2_approx(fminf(c * lg2_approx(r2), kExpClamp));
     }
+}
+
+// ---------------------------------------------------------------- packed FP32 pairs
+// A pair of floats held in one 64-bit register (PTX .b64) so that ptxas keeps
+// it in an aligned register pair and emits FADD2/FFMA2/FMUL2 without MOVs.
+typedef uint64_t f2x;
+__device__ __forceinline__ f2x pk(float a, float b) {
+    f2x r;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk(f2x r, float& a, float& b) {
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+}
+// a - (s, s): FADD2 with a broadcast scalar operand
+__device__ __forceinline__ f2x sub_bc(f2x a, float s) {
+    f2x d;
+    asm("{.reg .b64 t; mov.b64 t, {%2,%2}; sub.rn.f32x2 %0, %1, t;}" : "=l"(d) : "l"(a), "f"(s));
+    return d;
+}
+__device__ __forceinline__ f2x add2(f2x a, f2x b) {
+    f2x d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
+}
+__device__ __forceinline__ f2x fma2(f2x a, f2x b, f2x c) {
+    f2x d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+    return d;
+}
+__device__ __forceinline__ f2x mul2(f2x a, f2x b) {
+    f2x d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+    return d;
 }
 
 // ---------------------------------------------------------------- counter RNG (Q18)
