@@ -38,6 +38,7 @@ SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
 FP32_PEAK_TFLOPS = SM_COUNT * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12  # 74.4, derived
 MUFU_PER_CLK_SM = 16
 FLOP_PER_PAIR = 10  # 2D q = 0 pair: 2 sub + 2 fma (r^2) + 2 fma (acc), FMA = 2
+FLOP_PER_PAIR_COARSE = 11  # + the nu(v') weight
 
 
 # ------------------------------------------------------------------ distributed plumbing
@@ -200,9 +201,14 @@ def run_reference(args):
 
 
 def config_block(w, args):
-    return {"workload": f"{w.name}: BASELINE.json configs[1] (RGG n=65,536 -> LCC n={w.n}, S = hop<=2, "
-                        f"|S|={w.S.nnz}, q={w.q}, alpha={w.alpha}, dim={w.dim}, {w.sweeps} exact sweeps + energy)",
-            "n": w.n, "nnz_S": w.S.nnz, "sweeps_per_step": w.sweeps, "dim": w.dim, "q": w.q, "alpha": w.alpha,
+    if w.h == 0:
+        desc = (f"{w.name}: BASELINE.json configs[{int(w.name[3]) - 1 if w.name[3].isdigit() else '?'}] "
+                f"(n={w.n}, |S|={w.S.nnz}, q={w.q}, alpha={w.alpha}, dim={w.dim}, {w.sweeps} exact sweeps + energy)")
+    else:
+        desc = (f"{w.name}: multilevel mm_layout (n={w.n}, |S|={w.S.nnz}, q={w.q}, alpha={w.alpha}, dim={w.dim}, "
+                f"h={w.h}, {w.sweeps} sweeps/level, hierarchy build + prolongation + Eq.(3) sweeps + energy)")
+    return {"workload": desc, "n": w.n, "nnz_S": w.S.nnz, "sweeps_per_level": w.sweeps, "dim": w.dim, "q": w.q,
+            "alpha": w.alpha, "h": w.h,
             "l2": "flushed (256 MB write) between timed steps; per-step CUDA events",
             "parallelism": f"replicas x{args.gpus}"}
 
@@ -228,11 +234,12 @@ def run_gpu(args):
 
     with torch.cuda.stream(stream):
         S = mm.sset_to_device(w.S, dev)
-        x0 = mm.coords_to_device(w.x0, dev)
-        out = torch.empty_like(x0)
+        G = mm.graph_to_device(w.graph, dev) if w.h > 0 else None
+        x0 = mm.coords_to_device(w.x0, dev) if w.h == 0 else None
+        out = torch.empty((n, 2 if w.dim == 2 else 4), dtype=torch.float32, device=dev)
 
         def step():
-            return mm.layout(None, S, w.dim, w.alpha, w.q, 0, [K], w.seed, x_init=x0, out=out)
+            return mm.layout(G, S, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=x0, out=out)
 
         for _ in range(args.warmup):
             _, rep = step()
@@ -263,20 +270,24 @@ def run_gpu(args):
 
         # ---- e2e through the public API with host buffers
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
-        h_rp, h_col = pin(w.S.row_ptr.astype(np.int64)), pin(w.S.col.astype(np.int32))
-        h_d, h_w = pin(w.S.d.astype(np.float32)), pin(w.S.w.astype(np.float32))
-        h_x = pin(mm.coords_layout(w.x0))
+        hosts = [pin(w.S.row_ptr.astype(np.int64)), pin(w.S.col.astype(np.int32)),
+                 pin(w.S.d.astype(np.float32)), pin(w.S.w.astype(np.float32))]
+        if w.h == 0:
+            hosts.append(pin(mm.coords_layout(w.x0)))
+        else:
+            hosts += [pin(w.graph.row_ptr.astype(np.int64)), pin(w.graph.col.astype(np.int32))]
+        devs = [torch.empty_like(h, device=dev) for h in hosts]
         h_out = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
-        d_rp, d_col = torch.empty_like(h_rp, device=dev), torch.empty_like(h_col, device=dev)
-        d_d, d_w, d_x = torch.empty_like(h_d, device=dev), torch.empty_like(h_w, device=dev), torch.empty_like(h_x, device=dev)
-        Se = mm.DeviceSSet(d_rp, d_col, d_d, d_w)
-        h2d = sum(t.numel() * t.element_size() for t in (h_rp, h_col, h_d, h_w, h_x))
+        Se = mm.DeviceSSet(*devs[:4])
+        Ge = mm.DeviceGraph(devs[4], devs[5]) if w.h > 0 else None
+        xe = devs[4] if w.h == 0 else None
+        h2d = sum(t.numel() * t.element_size() for t in hosts)
         d2h = h_out.numel() * h_out.element_size() + 3 * 8  # layout + (stress, entropy, energy)
 
         def e2e_step():
-            for hd, dd in ((h_rp, d_rp), (h_col, d_col), (h_d, d_d), (h_w, d_w), (h_x, d_x)):
+            for hd, dd in zip(hosts, devs):
                 dd.copy_(hd, non_blocking=True)
-            y, r = mm.layout(None, Se, w.dim, w.alpha, w.q, 0, [K], w.seed, x_init=d_x, out=out)
+            y, r = mm.layout(Ge, Se, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=xe, out=out)
             h_out.copy_(y, non_blocking=True)
             return r
 
@@ -292,17 +303,28 @@ def run_gpu(args):
         torch.cuda.synchronize(dev)
         e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev2) / args.steps, dev)
 
-    units = sum_over_ranks(float(n * K), dev)
+    units = sum_over_ranks(float(rep["vertex_updates"]), dev)
     value = units / (ms_step / 1e3)
-    pairs_step = n * (n - 1) * K
-    kern = prof.get("repulse_exact", {"launches": 0, "total_ms": float("nan")})
+    pairs_step = rep["pair_interactions"]
+    kname = "repulse_exact" if w.h == 0 else "repulse_coarse"
+    kern = prof.get(kname, {"launches": 0, "total_ms": float("nan")})
     k_ms = kern["total_ms"] / max(kern["launches"], 1)
-    achieved_tflops = FLOP_PER_PAIR * n * (n - 1) / (k_ms / 1e3) / 1e12
+    # algorithmic pairs per launch: exact n(n-1) per sweep; coarse: the
+    # per-step pair count minus the exact coarsest level, averaged per launch
+    if w.h == 0:
+        pairs_launch = n * (n - 1)
+    else:
+        nL = rep["n_level"][-1]
+        pairs_launch = (pairs_step - nL * (nL - 1) * K) / max(kern["launches"] / args.steps, 1)
+    flop_pair = FLOP_PER_PAIR if w.h == 0 else FLOP_PER_PAIR_COARSE
+    if w.q != 0.0:
+        flop_pair += 3
+    achieved_tflops = flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
     step_share = {k: v["total_ms"] / max(dev_ms, 1e-9) for k, v in prof.items()}
     if rank != 0:
         return 0
     cpu = None
-    if ws == 1 and not args.no_cpu_baseline:
+    if ws == 1 and not args.no_cpu_baseline and w.h == 0:
         import oracle
 
         rows, cores = cpu_oracle_sample(w, target_s=args.cpu_s)
@@ -317,14 +339,16 @@ def run_gpu(args):
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": config_block(w, args),
         "pair_interactions_per_s": ws * pairs_step / (ms_step / 1e3),
-        "roofline": {"bound": "alu", "kernel": "repulse_exact (b)", "achieved": achieved_tflops,
+        "vertex_updates_per_step": rep["vertex_updates"], "pair_interactions_per_step": pairs_step,
+        "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved_tflops,
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_TFLOPS,
                      "traffic": None,
                      "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (DESIGN.md §5)",
-                     "flop_per_pair": FLOP_PER_PAIR, "pairs_per_launch": n * (n - 1),
+                     "flop_per_pair": flop_pair, "pairs_per_launch": pairs_launch,
                      "avg_launch_ms": k_ms,
                      "mufu_ceiling_frac": MUFU_PER_CLK_SM * FLOP_PER_PAIR / (2.0 * FP32_LANES),
-                     "pairs_per_s_kernel": n * (n - 1) / (k_ms / 1e3)},
+                     "pairs_per_s_kernel": pairs_launch / (k_ms / 1e3)},
+        "levels": rep["n_level"], "k_levels": rep["k_level"],
         "kernel_share_of_step": step_share,
         "kernels": prof,
         "cpu_baseline": cpu,

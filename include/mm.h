@@ -124,6 +124,8 @@ typedef struct {
     double rel_change;                  /* relative change of the last finest-level sweep */
     int64_t vertex_updates;             /* sum_l n_l * K_l */
     int64_t pair_interactions;          /* repulsion pairs evaluated (DESIGN.md §5 convention) */
+    int64_t coincident_pairs;           /* non-S ordered pairs at distance exactly 0 in the final
+                                           layout; they are left out of `entropy` (ln 0 undefined) */
 } mm_layout_report;
 
 /* ------------------------------------------------------------------ API */
@@ -195,7 +197,9 @@ MM_API mm_status mm_hierarchy_copy_level(const mm_hierarchy* h, int32_t level, i
  * sweeps there, then for l = L-1..0: prolongation (Q15) and
  * sweeps[min(l, nsweeps-1)] Eq.(3) sweeps with h' = min(h, L-l) (Q13); coarse
  * levels use S^l (Q7), level 0 uses S.  sweeps: HOST int32[nsweeps].
- * x_out: device, the finest layout.  rep: HOST report (nullable).  syncs. */
+ * x_out: device, the finest layout.  rep: HOST report (nullable); its energy
+ * leaves out pairs at distance exactly 0 and counts them (coincident_pairs),
+ * whereas mm_energy rejects them.  syncs. */
 MM_API mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, float alpha, float q, int h,
                     const int32_t* sweeps, int32_t nsweeps, uint64_t seed, int32_t n_stop,
                     const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream);

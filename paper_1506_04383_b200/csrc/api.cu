@@ -274,13 +274,17 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     return e;
 }
 
-// Energy with caller-provided stream; syncs.
+// Energy with caller-provided stream; syncs.  Pairs at distance exactly 0 are
+// skipped in both the all-pairs and the S sums and counted: *coinc_out (nullable)
+// receives the number of coincident non-S ORDERED pairs.  strict: such pairs
+// make Eq.(1) undefined (ln 0) and return MM_ERR_NONFINITE (mm_energy); the
+// layout report instead records the count next to the finite remainder.
 mm_status energy_core(const mm_sset* S, int dim, double alpha, double q, const float* x, double* out,
-                      cudaStream_t st) {
+                      cudaStream_t st, bool strict, int64_t* coinc_out) {
     const int32_t n = S->n;
     const double mean_row = (double)S->nnz / (double)n;
     EntropyPlan ep = plan_entropy(n);
-    const int nb_all = ep.tblocks * ep.P, nb_s = gather_blocks(n, mean_row);
+    const int nb_all = ep.nblocks, nb_s = gather_blocks(n, mean_row);
     const size_t bytes = al((size_t)nb_all * 8) + al((size_t)nb_s * 16) + al(16);
     DevBuf buf(bytes, st);
     if (!buf.p) { set_err("mm_energy: out of device memory (%zu B)", bytes); return MM_ERR_OUT_OF_MEMORY; }
@@ -289,7 +293,7 @@ mm_status energy_core(const mm_sset* S, int dim, double alpha, double q, const f
     double* ps = cv.take<double>((size_t)nb_s * 2);
     int32_t* coinc = cv.take<int32_t>(4);
     MM_CU(cudaMemsetAsync(coinc, 0, 16, st), "mm_energy memset");
-    MM_CU(launch_entropy_all(dim, q, n, x, ep, pa, coinc, st), "mm_energy entropy_all");
+    MM_CU(launch_entropy_all(dim, q, n, x, ep, pa, coinc, st), "mm_energy entropy_pairs");
     MM_CU(launch_energy_s(dim, q, n, S->row_ptr, S->col, S->d, S->w, x, mean_row, ps, coinc + 1, st),
           "mm_energy energy_s");
     std::vector<double> ha(nb_all), hs((size_t)nb_s * 2);
@@ -298,19 +302,22 @@ mm_status energy_core(const mm_sset* S, int dim, double alpha, double q, const f
     MM_CU(cudaMemcpyAsync(hs.data(), ps, (size_t)nb_s * 16, cudaMemcpyDeviceToHost, st), "mm_energy d2h");
     MM_CU(cudaMemcpyAsync(hc, coinc, 8, cudaMemcpyDeviceToHost, st), "mm_energy d2h");
     MM_CU(cudaStreamSynchronize(st), "mm_energy sync");
-    double sa = 0.0, ss = 0.0, sp = 0.0;
-    for (int b = 0; b < nb_all; ++b) sa += ha[b];
+    double su = 0.0, ss = 0.0, sp = 0.0;
+    for (int b = 0; b < nb_all; ++b) su += ha[b];
     for (int b = 0; b < nb_s; ++b) {
         ss += hs[(size_t)b * 2];
         sp += hs[(size_t)b * 2 + 1];
     }
-    const double diff = sa - sp;
-    const double entropy = (q == 0.0) ? 0.5 * (-0.5 * M_LN2) * diff : 0.5 * diff / q;
+    // sum over ordered non-S pairs / 2 = sum_{i<j} phi - 1/2 sum_S phi
+    const double diff = su - 0.5 * sp;
+    const double entropy = (q == 0.0) ? (-0.5 * M_LN2) * diff : diff / q;
     out[0] = 0.5 * ss;
     out[1] = entropy;
     out[2] = out[0] + alpha * out[1];
-    if (hc[0] > hc[1]) {
-        set_err("mm_energy: %d coincident non-S ordered pair(s): ln 0 is undefined (Eq.(1))", hc[0] - hc[1]);
+    const int64_t nonS = 2 * (int64_t)hc[0] - hc[1];
+    if (coinc_out) *coinc_out = nonS;
+    if (strict && nonS > 0) {
+        set_err("mm_energy: %lld coincident non-S ordered pair(s): ln 0 is undefined (Eq.(1))", (long long)nonS);
         return MM_ERR_NONFINITE;
     }
     if (!isfinite(out[2])) {
@@ -414,7 +421,7 @@ mm_status mm_energy(const mm_sset* S, int dim, double alpha, double q, const flo
     if ((s = check_dim_q(dim, q, "mm_energy")) != MM_OK) return s;
     if ((s = check_x(x, dim, "x", "mm_energy")) != MM_OK) return s;
     if (!out) { set_err("mm_energy: out is NULL"); return MM_ERR_INVALID_ARGUMENT; }
-    return energy_core(S, dim, alpha, q, x, out, (cudaStream_t)stream);
+    return energy_core(S, dim, alpha, q, x, out, (cudaStream_t)stream, true, nullptr);
 }
 
 int64_t mm_launch_count(void) { return g_launches.load(); }
@@ -965,7 +972,9 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
         if (hs.flags & 1) { set_err("mm_layout: non-finite coordinate produced"); return MM_ERR_NONFINITE; }
     }
     double en[3] = {0, 0, 0};
-    s = energy_core(S, dim, alpha, q, x_out, en, ls);
+    int64_t coinc = 0;
+    s = energy_core(S, dim, alpha, q, x_out, en, ls, false, &coinc);
+    R.coincident_pairs = coinc;
     R.stress = en[0];
     R.entropy = en[1];
     R.energy = en[2];

@@ -212,13 +212,17 @@ __global__ void __launch_bounds__(kGBlock) k_energy_s(int32_t n, const int64_t* 
                 const float dz = xi.z - xj.z;
                 r2 = fmaf(dz, dz, r2);
             }
-            zc += (r2 == 0.f) ? 1 : 0;
             const float dist = sqrtf(r2);
             const float dev = dist - __ldg(d + e);
             st = fmaf(__ldg(w + e) * dev, dev, st);
-            const float l = lg2_approx(r2 + kEps2);
-            if constexpr (!QPOW) ph += l;
-            else ph += ex2_approx(fminf(cq * l, kExpClamp));
+            // same per-pair transform as k_entropy_tri; coincident pairs skipped and counted
+            if (r2 == 0.f) {
+                ++zc;
+            } else {
+                const float l = lg2_approx(fmaxf(r2, 1e-18f));  // same r^2 floor as k_entropy_tri
+                if constexpr (!QPOW) ph += l;
+                else ph += ex2_approx(fminf(cq * l, kExpClamp));
+            }
         }
     }
     double a0 = st, a1 = ph;

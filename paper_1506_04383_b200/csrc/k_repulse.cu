@@ -50,8 +50,8 @@ __device__ __forceinline__ f2x inv_pair(f2x r2, float cexp) {
     }
 }
 
-template <int DIM, bool QPOW, bool COARSE, int T>
-__global__ void __launch_bounds__(kBlock) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
+template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
                                                     const float4* __restrict__ rep_hi,
                                                     const float4* __restrict__ rep_lo,
                                                     const int32_t* __restrict__ anc, float cexp, Sched sch,
@@ -146,7 +146,8 @@ __global__ void __launch_bounds__(kBlock) k_repulse(int32_t n_tgt, const float* 
                         if constexpr (COARSE) dz = sub_bc(dz, lz);
                         r2 = fma2(dz, dz, r2);
                     }
-                    f2x inv = (gg % 2 == 0) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+                    // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
+                    f2x inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
                     if constexpr (COARSE) {
                         const int32_t j = (int32_t)(t0 + jj);
                         inv = mul2(inv, pk(j == hi[2 * gg] ? 0.f : nu, j == hi[2 * gg + 1] ? 0.f : nu));
@@ -180,55 +181,132 @@ __global__ void __launch_bounds__(kBlock) k_repulse(int32_t n_tgt, const float* 
     }
 }
 
-// All-pairs entropy for mm_energy: per target, sum over j != i of phi_q(r)
-// in the form  q = 0: sum lg2(r^2 + eps)   (phi_0 = -ln r = -(ln 2 / 2) lg2 r^2)
-//              q > 0: sum 2^(-q/2 lg2(r^2 + eps))   (phi_q = r^-q / q)
-// plus a count of exactly coincident pairs (j != i).  FP32 per thread and
-// tile, FP64 across tiles and threads, written per CTA.
+// All-pairs entropy for mm_energy over UNORDERED pairs i < j (the ordered sum
+// of Eq.(1) in the S form is  1/2 sum_{i != j} phi - 1/2 sum_i sum_{S_i} phi
+// = sum_{i<j} phi - 1/2 sum_S phi, valid for asymmetric S too):
+//   q = 0: sum lg2(r^2), two pairs per MUFU via lg2(a) + lg2(b) = lg2(a b)
+//          (phi_0 = -ln r = -(ln 2 / 2) lg2 r^2)
+//   q > 0: sum 2^(-q/2 lg2 r^2)      (phi_q = r^-q / q)
+// Exactly coincident pairs (r = 0) are skipped and counted.  Triangular
+// persistent schedule: target block tb (TPB targets) pairs with source tiles
+// from its own first tile on; the unit space is split into G equal ranges and
+// every CTA writes one FP64 partial (FP32 within a tile, FP64 across tiles).
+constexpr float kR2Floor = 1e-18f;  // r^2 clamp: keeps products of two r^2 normal
+
+template <int DIM>
+__device__ __forceinline__ f2x entropy_r2(f2x X, f2x Y, f2x Z, const float4& sv) {
+    const f2x dx = sub_bc(X, sv.x), dy = sub_bc(Y, sv.y);
+    f2x r2 = mul2(dx, dx);
+    r2 = fma2(dy, dy, r2);
+    if constexpr (DIM == 3) {
+        const f2x dz = sub_bc(Z, sv.z);
+        r2 = fma2(dz, dz, r2);
+    }
+    return r2;
+}
+
+// phi-sum contribution of two pairs with (clamped) r^2 = a, b:
+// q = 0: lg2(a) + lg2(b) = lg2(a b)  (one MUFU);  q > 0: 2^(cq lg2 a) + 2^(cq lg2 b)
+template <bool QPOW>
+__device__ __forceinline__ float entropy_phi2(float a, float b, float cq) {
+    if constexpr (!QPOW) {
+        return lg2_approx(a * b);
+    } else {
+        return ex2_approx(fminf(cq * lg2_approx(a), kExpClamp)) + ex2_approx(fminf(cq * lg2_approx(b), kExpClamp));
+    }
+}
+
 template <int DIM, bool QPOW>
-__global__ void __launch_bounds__(kBlock) k_entropy_all(int32_t n, const float* __restrict__ x, float cq,
-                                                        int32_t chunk, double* __restrict__ partial,
+__global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* __restrict__ x, float cq,
+                                                        TriSched ts, double* __restrict__ partial,
                                                         int32_t* __restrict__ coinc) {
+    constexpr int T = 4, G = 2, TPB = kBlock * T;
+    constexpr int stride = DIM == 2 ? 2 : 4;
     __shared__ float4 sm[kBlock];
     __shared__ double red[kBlock / 32];
     __shared__ int32_t redc[kBlock / 32];
     const int tid = threadIdx.x;
-    const int64_t i = (int64_t)blockIdx.x * kBlock + tid;
-    const int64_t ci = i < n ? i : n - 1;
-    const float4 xi = load_x<DIM>(x, ci);
+    const int32_t g = blockIdx.x;
+    const int64_t u0 = (int64_t)g * ts.U / ts.G, u1 = (int64_t)(g + 1) * ts.U / ts.G;
     double dacc = 0.0;
     int32_t zc = 0;
-    const int64_t s_begin = (int64_t)blockIdx.y * chunk;
-    const int64_t s_end = min((int64_t)n, s_begin + chunk);
-    for (int64_t t0 = s_begin; t0 < s_end; t0 += kBlock) {
-        const int cnt = (int)min((int64_t)kBlock, s_end - t0);
-        __syncthreads();
-        if (tid < cnt) sm[tid] = load_x<DIM>(x, t0 + tid);
-        __syncthreads();
-        float acc = 0.f;
-#pragma unroll 4
-        for (int jj = 0; jj < cnt; ++jj) {
-            const float4 s = sm[jj];
-            const float dx = xi.x - s.x, dy = xi.y - s.y;
-            float r2 = fmaf(dx, dx, 0.f);
-            r2 = fmaf(dy, dy, r2);
-            if constexpr (DIM == 3) {
-                const float dz = xi.z - s.z;
-                r2 = fmaf(dz, dz, r2);
-            }
-            const bool self = (t0 + jj) == i;
-            zc += (r2 == 0.f && !self) ? 1 : 0;
-            const float l = lg2_approx(r2 + kEps2);
-            float v;
-            if constexpr (!QPOW) v = l;
-            else v = ex2_approx(fminf(cq * l, kExpClamp));
-            acc += self ? 0.f : v;
+    for (int64_t u = u0; u < u1;) {
+        // target block containing unit u: largest tb with prefix(tb) <= u
+        int32_t lo = 0, hi = ts.TB - 1;
+        while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) >> 1;
+            if (tri_prefix(mid, ts) <= u) lo = mid; else hi = mid - 1;
         }
-        dacc += (double)acc;
-    }
-    if (i >= n) {
-        dacc = 0.0;
-        zc = 0;
+        const int32_t tb = lo;
+        const int64_t pre = tri_prefix(tb, ts);
+        const int32_t first_tile = tb * (TPB / kBlock);
+        const int64_t seg_end = min(u1, tri_prefix(tb + 1, ts));
+        const int32_t tile0 = first_tile + (int32_t)(u - pre), tile1 = first_tile + (int32_t)(seg_end - pre);
+        const int64_t base = (int64_t)tb * TPB;
+        f2x X[G], Y[G], Z[G];
+        int32_t ti[T];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+            const int64_t ia = base + (2 * gg) * kBlock + tid, ib = base + (2 * gg + 1) * kBlock + tid;
+            ti[2 * gg] = (int32_t)ia;
+            ti[2 * gg + 1] = (int32_t)ib;
+            const int64_t ca = ia < n ? ia : n - 1, cb = ib < n ? ib : n - 1;
+            const float* pa = x + ca * stride;
+            const float* pb = x + cb * stride;
+            X[gg] = pk(__ldg(pa), __ldg(pb));
+            Y[gg] = pk(__ldg(pa + 1), __ldg(pb + 1));
+            Z[gg] = (DIM == 3) ? pk(__ldg(pa + 2), __ldg(pb + 2)) : 0ull;
+        }
+        for (int32_t tile = tile0; tile < tile1; ++tile) {
+            const int64_t t0 = (int64_t)tile * kBlock;
+            const int cnt = (int)min((int64_t)kBlock, (int64_t)n - t0);
+            __syncthreads();
+            if (tid < cnt) sm[tid] = load_x<DIM>(x, t0 + tid);
+            __syncthreads();
+            // tiles overlapping the target block need the i < j mask (and targets >= n)
+            const bool diag = (t0 < base + TPB) || (base + TPB > n);
+            float acc = 0.f;
+            int32_t zt = 0;
+            if (!diag) {
+#pragma unroll 4
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const float4 sv = sm[jj];
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        float ra, rb;
+                        upk(entropy_r2<DIM>(X[gg], Y[gg], Z[gg], sv), ra, rb);
+                        zt += (ra == 0.f) + (rb == 0.f);
+                        acc += entropy_phi2<QPOW>(fmaxf(ra, kR2Floor), fmaxf(rb, kR2Floor), cq);
+                    }
+                }
+            } else {
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const float4 sv = sm[jj];
+                    const int32_t j = (int32_t)(t0 + jj);
+#pragma unroll
+                    for (int gg = 0; gg < G; ++gg) {
+                        float ra, rb;
+                        upk(entropy_r2<DIM>(X[gg], Y[gg], Z[gg], sv), ra, rb);
+                        const bool va = j > ti[2 * gg] && ti[2 * gg] < n;
+                        const bool vb = j > ti[2 * gg + 1] && ti[2 * gg + 1] < n;
+                        zt += (va && ra == 0.f) + (vb && rb == 0.f);
+                        // masked pairs: r^2 = 1 contributes lg2(1) = 0 (q = 0); q > 0 masks the term
+                        const float pa = va ? fmaxf(ra, kR2Floor) : 1.f, pb = vb ? fmaxf(rb, kR2Floor) : 1.f;
+                        if constexpr (!QPOW) {
+                            acc += entropy_phi2<false>(pa, pb, cq);
+                        } else {
+                            acc += (va ? entropy_phi2<true>(pa, 1.f, cq) - 1.f : 0.f) +
+                                   (vb ? entropy_phi2<true>(pb, 1.f, cq) - 1.f : 0.f);
+                        }
+                    }
+                }
+            }
+            // coincident pairs entered with r^2 = kR2Floor: remove their contribution
+            if (zt) acc -= (float)zt * entropy_phi2<QPOW>(kR2Floor, 1.f, cq) - (QPOW ? (float)zt : 0.f);
+            zc += zt;
+            dacc += (double)acc;
+        }
+        u = seg_end;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -247,7 +325,7 @@ __global__ void __launch_bounds__(kBlock) k_entropy_all(int32_t n, const float* 
             s += red[w];
             c += redc[w];
         }
-        partial[(int64_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+        partial[g] = s;
         if (c) atomicAdd(coinc, c);
     }
 }
@@ -329,28 +407,31 @@ int repulse_targets_per_block(int dim) { return kBlock * targets_per_thread(dim)
 
 EntropyPlan plan_entropy(int32_t n) {
     EntropyPlan p;
-    p.tblocks = (n + kBlock - 1) / kBlock;
-    int P = (sm_count() * 6 + p.tblocks - 1) / p.tblocks;
-    P = std::max(1, std::min(P, std::max(1, n / (2 * kBlock))));
-    int64_t chunk = ((int64_t)n + P - 1) / P;
-    chunk = ((chunk + kBlock - 1) / kBlock) * kBlock;
-    p.chunk = (int32_t)std::max<int64_t>(chunk, kBlock);
-    p.P = (int)(((int64_t)n + p.chunk - 1) / p.chunk);
+    TriSched& t = p.ts;
+    const int TPB = kBlock * 4;
+    t.TB = (int32_t)((n + TPB - 1) / TPB);
+    t.Ub = (int32_t)((n + kBlock - 1) / kBlock);
+    t.c = TPB / kBlock;
+    t.U = tri_prefix(t.TB, t);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_entropy_tri<2, false>, kBlock, 0);
+    t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), t.U));
+    p.nblocks = t.G;
     return p;
 }
 
 cudaError_t launch_entropy_all(int dim, double q, int32_t n, const float* x, const EntropyPlan& p,
                                double* partial, int32_t* coinc, cudaStream_t st) {
-    dim3 grid(p.tblocks, p.P);
     const float cq = (float)(-q * 0.5);
-    LaunchScope ls("entropy_all", st);
+    LaunchScope ls("entropy_pairs", st);
     const bool qpow = q != 0.0;
+    const int G = p.ts.G;
     if (dim == 2) {
-        if (qpow) k_entropy_all<2, true><<<grid, kBlock, 0, st>>>(n, x, cq, p.chunk, partial, coinc);
-        else k_entropy_all<2, false><<<grid, kBlock, 0, st>>>(n, x, cq, p.chunk, partial, coinc);
+        if (qpow) k_entropy_tri<2, true><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
+        else k_entropy_tri<2, false><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
     } else {
-        if (qpow) k_entropy_all<3, true><<<grid, kBlock, 0, st>>>(n, x, cq, p.chunk, partial, coinc);
-        else k_entropy_all<3, false><<<grid, kBlock, 0, st>>>(n, x, cq, p.chunk, partial, coinc);
+        if (qpow) k_entropy_tri<3, true><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
+        else k_entropy_tri<3, false><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
     }
     return cudaGetLastError();
 }

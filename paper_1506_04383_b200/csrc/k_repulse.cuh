@@ -24,10 +24,19 @@ struct RepulsePlan {
     Sched sch;
     int slots = 1;     // max partial slots per target (size of the partial buffer / n)
 };
+// Triangular schedule of the unordered-pair entropy kernel: target block tb
+// owns source tiles [tb*c, Ub) (c = tiles per target block); prefix(tb) =
+// sum_{t<tb} (Ub - t c) = tb Ub - c tb (tb-1) / 2.
+struct TriSched {
+    int64_t U = 1;
+    int32_t Ub = 1, TB = 1, c = 1, G = 1;
+};
+__host__ __device__ __forceinline__ int64_t tri_prefix(int32_t tb, const TriSched& s) {
+    return (int64_t)tb * s.Ub - (int64_t)s.c * tb * (tb - 1) / 2;
+}
 struct EntropyPlan {
-    int tblocks = 1;
-    int P = 1;
-    int32_t chunk = 0;
+    TriSched ts;
+    int nblocks = 1;   // CTAs = FP64 partials
 };
 
 RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, bool qpow);

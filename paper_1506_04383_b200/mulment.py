@@ -64,7 +64,8 @@ class mm_layout_report(ctypes.Structure):
     _fields_ = [("levels", ctypes.c_int32), ("n_level", ctypes.c_int32 * MM_MAX_LEVELS),
                 ("k_level", ctypes.c_int32 * MM_MAX_LEVELS), ("stress", ctypes.c_double),
                 ("entropy", ctypes.c_double), ("energy", ctypes.c_double), ("rel_change", ctypes.c_double),
-                ("vertex_updates", ctypes.c_int64), ("pair_interactions", ctypes.c_int64)]
+                ("vertex_updates", ctypes.c_int64), ("pair_interactions", ctypes.c_int64),
+                ("coincident_pairs", ctypes.c_int64)]
 
 
 class mm_kernel_profile(ctypes.Structure):
@@ -319,7 +320,7 @@ def layout(g: Optional[DeviceGraph], S: DeviceSSet, dim: int, alpha: float, q: f
     r = {"levels": rep.levels, "n_level": list(rep.n_level[:rep.levels]),
          "k_level": list(rep.k_level[:rep.levels]), "stress": rep.stress, "entropy": rep.entropy,
          "energy": rep.energy, "rel_change": rep.rel_change, "vertex_updates": rep.vertex_updates,
-         "pair_interactions": rep.pair_interactions}
+         "pair_interactions": rep.pair_interactions, "coincident_pairs": rep.coincident_pairs}
     return out, r
 
 
