@@ -756,8 +756,51 @@ bool graphs_enabled() {
     return !(e && e[0] && e[0] != '0') && !g_prof_on.load();
 }
 
+// Instantiated CUDA graphs of K-sweep sequences, keyed by every value the
+// captured launches depend on (pointers, sizes, parameters).  A hit relaunches
+// the executable graph; capture + instantiate is paid once per distinct key.
+struct GraphKey {
+    const void* p[16];
+    int64_t v[8];
+    float f[2];
+    bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int64_t kernels;
+    uint64_t stamp;
+};
+std::mutex g_graph_mu;
+std::vector<GraphEntry> g_graphs;
+uint64_t g_graph_clock = 0;
+constexpr size_t kGraphCacheMax = 16;
+
+GraphKey make_key(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* src,
+                  const float* bufA, const float* bufB, int32_t K, const mm_sweep_stats* stats, const SweepBufs& sb,
+                  cudaStream_t st) {
+    GraphKey k;
+    memset(&k, 0, sizeof(k));
+    (void)st;  // an executable graph may be launched into any stream
+    const void* ps[16] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
+                          sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child};
+    memcpy(k.p, ps, sizeof(ps));
+    k.v[0] = S->n;
+    k.v[1] = S->nnz;
+    k.v[2] = dim;
+    k.v[3] = K;
+    k.v[4] = ap ? ap->k : -1;
+    k.v[5] = (int64_t)(uintptr_t)(ap ? ap->parent : nullptr);
+    k.v[6] = (int64_t)(uintptr_t)sb.cptr;
+    k.v[7] = (int64_t)(uintptr_t)sb.mem;
+    k.f[0] = alpha;
+    k.f[1] = q;
+    return k;
+}
+
 // Runs K sweeps ping-ponging between bufA/bufB starting from src; returns the
-// buffer holding the result.  Optionally captured into one CUDA graph.
+// buffer holding the result.  With graphs enabled the sequence is captured
+// once into a CUDA graph (cached) and relaunched.
 cudaError_t run_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* src,
                        float* bufA, float* bufB, int32_t K, mm_sweep_stats* stats, const SweepBufs& sb,
                        cudaStream_t st, const float** result) {
@@ -765,32 +808,62 @@ cudaError_t run_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm
         *result = src;
         return cudaSuccess;
     }
-    const bool use_graph = graphs_enabled() && K > 1;
-    cudaGraph_t graph = nullptr;
-    if (use_graph) {
-        cudaError_t e = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
-        if (e != cudaSuccess) return e;
-    }
+    // result buffer of the ping-pong (independent of capture)
     const float* cur = src;
-    cudaError_t err = cudaSuccess;
-    for (int32_t s = 0; s < K && err == cudaSuccess; ++s) {
-        float* dst = (cur == bufA) ? bufB : bufA;
-        err = sweep_core(S, dim, alpha, q, ap, cur, dst, stats, sb, st);
-        cur = dst;
-    }
-    if (use_graph) {
-        cudaError_t e = cudaStreamEndCapture(st, &graph);
-        if (err == cudaSuccess) err = e;
-        if (err == cudaSuccess) {
-            cudaGraphExec_t exec = nullptr;
-            err = cudaGraphInstantiate(&exec, graph, 0);
-            if (err == cudaSuccess) err = cudaGraphLaunch(exec, st);
-            if (err == cudaSuccess) err = cudaStreamSynchronize(st);
-            if (exec) cudaGraphExecDestroy(exec);
-        }
-        if (graph) cudaGraphDestroy(graph);
-    }
+    for (int32_t s = 0; s < K; ++s) cur = (cur == bufA) ? bufB : bufA;
     *result = cur;
+    const bool use_graph = graphs_enabled() && K > 1 && st != nullptr;
+    if (!use_graph) {
+        const float* c = src;
+        for (int32_t s = 0; s < K; ++s) {
+            float* dst = (c == bufA) ? bufB : bufA;
+            cudaError_t err = sweep_core(S, dim, alpha, q, ap, c, dst, stats, sb, st);
+            if (err != cudaSuccess) return err;
+            c = dst;
+        }
+        return cudaSuccess;
+    }
+    const GraphKey key = make_key(S, dim, alpha, q, ap, src, bufA, bufB, K, stats, sb, st);
+    {
+        std::lock_guard<std::mutex> g(g_graph_mu);
+        for (auto& e : g_graphs) {
+            if (e.key == key) {
+                e.stamp = ++g_graph_clock;
+                g_launches.fetch_add(e.kernels, std::memory_order_relaxed);
+                return cudaGraphLaunch(e.exec, st);
+            }
+        }
+    }
+    const int64_t l0 = g_launches.load();
+    cudaError_t err = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+    if (err != cudaSuccess) return err;
+    const float* c = src;
+    for (int32_t s = 0; s < K && err == cudaSuccess; ++s) {
+        float* dst = (c == bufA) ? bufB : bufA;
+        err = sweep_core(S, dim, alpha, q, ap, c, dst, stats, sb, st);
+        c = dst;
+    }
+    cudaGraph_t graph = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(st, &graph);
+    if (err == cudaSuccess) err = e2;
+    cudaGraphExec_t exec = nullptr;
+    if (err == cudaSuccess) err = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (err != cudaSuccess) {
+        if (exec) cudaGraphExecDestroy(exec);
+        return err;
+    }
+    err = cudaGraphLaunch(exec, st);
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    if (g_graphs.size() >= kGraphCacheMax) {
+        size_t victim = 0;
+        for (size_t i = 1; i < g_graphs.size(); ++i)
+            if (g_graphs[i].stamp < g_graphs[victim].stamp) victim = i;
+        cudaDeviceSynchronize();  // the victim may still be running
+        cudaGraphExecDestroy(g_graphs[victim].exec);
+        g_graphs.erase(g_graphs.begin() + victim);
+    }
+    g_graphs.push_back(GraphEntry{key, exec, g_launches.load() - l0, ++g_graph_clock});
     return err;
 }
 
@@ -819,14 +892,19 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
     const int st_w = stride_of(dim);
     const size_t xbytes = (size_t)n0 * st_w * sizeof(float);
     cudaStream_t us = (cudaStream_t)stream;
-    cudaStream_t ls = nullptr;
     cudaEvent_t ev = nullptr;
-    MM_CU(cudaStreamCreateWithFlags(&ls, cudaStreamNonBlocking), "mm_layout stream");
+    // the driver's own non-blocking stream (persistent, so that stream-ordered
+    // workspace reuse and the graph cache see the same addresses call after call)
+    static std::mutex s_stream_mu;
+    static cudaStream_t s_ls = nullptr;
+    std::lock_guard<std::mutex> stream_lock(s_stream_mu);
+    if (!s_ls) MM_CU(cudaStreamCreateWithFlags(&s_ls, cudaStreamNonBlocking), "mm_layout stream");
+    cudaStream_t ls = s_ls;
     struct StreamGuard {
         cudaStream_t s;
         cudaEvent_t e;
         ~StreamGuard() {
-            if (s) { cudaStreamSynchronize(s); cudaStreamDestroy(s); }
+            if (s) cudaStreamSynchronize(s);
             if (e) cudaEventDestroy(e);
         }
     } guard{ls, nullptr};
