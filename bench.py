@@ -321,6 +321,16 @@ def run_gpu(args):
         flop_pair += 3
     achieved_tflops = flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
     step_share = {k: v["total_ms"] / max(dev_ms, 1e-9) for k, v in prof.items()}
+    gpu_ms = sum(v["total_ms"] for v in prof.values())
+    gpu_share = {k: v["total_ms"] / max(gpu_ms, 1e-9) for k, v in prof.items()}
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tj = json.load(f)
+        if kname in tj and w.name in tj[kname].get("workload", ""):
+            traffic = tj[kname]["bytes"]
+    except (OSError, ValueError, KeyError):
+        traffic = None
     if rank != 0:
         return 0
     cpu = None
@@ -342,7 +352,7 @@ def run_gpu(args):
         "vertex_updates_per_step": rep["vertex_updates"], "pair_interactions_per_step": pairs_step,
         "roofline": {"bound": "alu", "kernel": kname, "achieved": achieved_tflops,
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_TFLOPS,
-                     "traffic": None,
+                     "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
                      "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (DESIGN.md §5)",
                      "flop_per_pair": flop_pair, "pairs_per_launch": pairs_launch,
                      "avg_launch_ms": k_ms,
@@ -350,6 +360,7 @@ def run_gpu(args):
                      "pairs_per_s_kernel": pairs_launch / (k_ms / 1e3)},
         "levels": rep["n_level"], "k_levels": rep["k_level"],
         "kernel_share_of_step": step_share,
+        "kernel_share_of_gpu_time": gpu_share,
         "kernels": prof,
         "cpu_baseline": cpu,
         "e2e": {"value": units / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,

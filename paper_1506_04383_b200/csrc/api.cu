@@ -248,8 +248,6 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, nullptr, p, sb.part, st);
     }
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(sb.flags, 0, sizeof(int32_t), st);
-    if (e != cudaSuccess) return e;
     GatherArgs ga;
     ga.n = n;
     ga.rp = S->row_ptr;
@@ -268,10 +266,9 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     ga.x_out = x_out;
     ga.stat_partial = sb.stat_partial;
     ga.flags = sb.flags;
-    e = launch_gather(dim, ga, mean_row, st);
-    if (e != cudaSuccess) return e;
-    if (stats) e = launch_stats_final(sb.stat_partial, gather_blocks(n, mean_row), sb.flags, stats, st);
-    return e;
+    ga.ticket = sb.flags + 1;
+    ga.stats = stats;
+    return launch_gather(dim, ga, mean_row, st);
 }
 
 // Energy with caller-provided stream; syncs.  Pairs at distance exactly 0 are
@@ -409,6 +406,7 @@ mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const mm_app
         set_err("mm_sweep: workspace carving failed");
         return MM_ERR_INVALID_ARGUMENT;
     }
+    MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), st), "mm_sweep memset");
     if (ap) MM_CU(prepare_approx(n, ap, sb, st), "mm_sweep prepare_approx");
     MM_CU(sweep_core(S, dim, alpha, q, ap, x_in, x_out, stats, sb, st), "mm_sweep");
     return MM_OK;
@@ -928,6 +926,7 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
         mm_sweep_stats* dstats = cv.take<mm_sweep_stats>(1);
         SweepBufs sb;
         if (!carve_sweep(cv, n0, dim, 0, false, mean_row, sb)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+        MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
         MM_CU(cudaMemsetAsync(dstats, 0, sizeof(mm_sweep_stats), ls), "mm_layout memset");
         // choose the first destination so that the last sweep lands in x_out
         const float* src = x_init;
@@ -1004,6 +1003,7 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
             Carver wc((char*)buf.p + ws_off, need - ws_off);
             SweepBufs sb;
             if (!carve_sweep(wc, nL, dim, 0, false, 1.0, sb)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+            MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
             const float* res = nullptr;
             MM_CU(run_sweeps(&SL, dim, alpha, q, nullptr, xa, xb, xa, K_of(L), dstats, sb, ls, &res), "mm_layout coarsest");
             R.n_level[L] = nL;
@@ -1031,6 +1031,7 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
                 Carver wl((char*)buf.p + ws_off, need - ws_off);
                 SweepBufs sbl;
                 if (!carve_sweep(wl, nf, dim, ap.k, true, 1.0, sbl)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+                MM_CU(cudaMemsetAsync(sbl.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
                 MM_CU(prepare_approx(nf, &ap, sbl, ls), "mm_layout prepare_approx");
                 float* other = (cur == xa) ? xb : xa;
                 MM_CU(run_sweeps(&Sl, dim, alpha, q, &ap, cur, other, (float*)cur, K_of(l), dstats, sbl, ls, &res),

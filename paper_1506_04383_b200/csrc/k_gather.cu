@@ -55,64 +55,67 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
 template <int DIM, bool QPOW, int G>
 __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
     const int lg = threadIdx.x & (G - 1);
-    const int64_t i = ((int64_t)blockIdx.x * kGBlock + threadIdx.x) / G;
+    constexpr int VPB = kGBlock / G;  // vertices per block iteration
     double v_dx2 = 0.0, v_x2 = 0.0, v_st = 0.0;
-    const bool valid = i < a.n;
-    float4 xi = make_float4(0.f, 0.f, 0.f, 0.f);
-    float rho = 0.f, st = 0.f;
-    float4 A = make_float4(0.f, 0.f, 0.f, 0.f), C = A;
-    if (valid) {
-        xi = load_x<DIM>(a.x, i);
-        const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];
-        for (int64_t e = e0 + lg; e < e1; e += G) {
-            const int32_t j = __ldg(a.col + e);
-            const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);
-            const float4 xj = load_x<DIM>(a.x, j);
-            const float dx = xi.x - xj.x, dy = xi.y - xj.y;
-            float r2 = fmaf(dx, dx, kEps2);
-            r2 = fmaf(dy, dy, r2);
-            float dz = 0.f;
-            if constexpr (DIM == 3) {
-                dz = xi.z - xj.z;
-                r2 = fmaf(dz, dz, r2);
+    // grid-stride over vertex chunks: a fixed number of CTAs -> a fixed,
+    // small number of FP64 partials, each accumulated in a fixed order
+    for (int64_t vb = (int64_t)blockIdx.x * VPB; vb < a.n; vb += (int64_t)gridDim.x * VPB) {
+        const int64_t i = vb + threadIdx.x / G;
+        const bool valid = i < a.n;
+        float4 xi = make_float4(0.f, 0.f, 0.f, 0.f);
+        float rho = 0.f, st = 0.f;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f), C = A;
+        if (valid) {
+            xi = load_x<DIM>(a.x, i);
+            const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];
+            for (int64_t e = e0 + lg; e < e1; e += G) {
+                const int32_t j = __ldg(a.col + e);
+                const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);
+                const float4 xj = load_x<DIM>(a.x, j);
+                const float dx = xi.x - xj.x, dy = xi.y - xj.y;
+                float r2 = fmaf(dx, dx, kEps2);
+                r2 = fmaf(dy, dy, r2);
+                float dz = 0.f;
+                if constexpr (DIM == 3) {
+                    dz = xi.z - xj.z;
+                    r2 = fmaf(dz, dz, r2);
+                }
+                // S-pair r-value, removed from the all-pairs / representative sum
+                const float inv = inv_pow<QPOW>(r2, cexp);
+                C.x = fmaf(dx, inv, C.x);
+                C.y = fmaf(dy, inv, C.y);
+                if constexpr (DIM == 3) C.z = fmaf(dz, inv, C.z);
+                // attraction: w (x_j + d (x_i - x_j)/|x_i - x_j|)
+                const float rinv = rsqrt_approx(r2);
+                const float dist = r2 * rinv;
+                const float s = dd * rinv;
+                rho += ww;
+                A.x = fmaf(ww, fmaf(s, dx, xj.x), A.x);
+                A.y = fmaf(ww, fmaf(s, dy, xj.y), A.y);
+                if constexpr (DIM == 3) A.z = fmaf(ww, fmaf(s, dz, xj.z), A.z);
+                const float dev = dist - dd;
+                st = fmaf(ww * dev, dev, st);
             }
-            // S-pair r-value, removed from the all-pairs / representative sum
-            const float inv = inv_pow<QPOW>(r2, cexp);
-            C.x = fmaf(dx, inv, C.x);
-            C.y = fmaf(dy, inv, C.y);
-            if constexpr (DIM == 3) C.z = fmaf(dz, inv, C.z);
-            // attraction: w (x_j + d (x_i - x_j)/|x_i - x_j|)
-            const float rinv = rsqrt_approx(r2);
-            const float dist = r2 * rinv;
-            const float s = dd * rinv;
-            rho += ww;
-            A.x = fmaf(ww, fmaf(s, dx, xj.x), A.x);
-            A.y = fmaf(ww, fmaf(s, dy, xj.y), A.y);
-            if constexpr (DIM == 3) A.z = fmaf(ww, fmaf(s, dz, xj.z), A.z);
-            const float dev = dist - dd;
-            st = fmaf(ww * dev, dev, st);
-        }
-        if (a.parent != nullptr) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
-            const int32_t p = __ldg(a.parent + i);
-            const int32_t c0 = __ldg(a.child_ptr + p), c1 = __ldg(a.child_ptr + p + 1);
-            for (int32_t c = c0 + lg; c < c1; c += G) {
-                const int32_t j = __ldg(a.child + c);
-                if (j != i) r_value<DIM, QPOW>(xi, load_x<DIM>(a.x, j), cexp, C, -1.f);
+            if (a.parent != nullptr) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
+                const int32_t p = __ldg(a.parent + i);
+                const int32_t c0 = __ldg(a.child_ptr + p), c1 = __ldg(a.child_ptr + p + 1);
+                for (int32_t c = c0 + lg; c < c1; c += G) {
+                    const int32_t j = __ldg(a.child + c);
+                    if (j != i) r_value<DIM, QPOW>(xi, load_x<DIM>(a.x, j), cexp, C, -1.f);
+                }
             }
         }
-    }
-    // all lanes of the warp take part in the shuffles
-    rho = group_sum<G>(rho);
-    st = group_sum<G>(st);
-    A.x = group_sum<G>(A.x);
-    A.y = group_sum<G>(A.y);
-    C.x = group_sum<G>(C.x);
-    C.y = group_sum<G>(C.y);
-    if constexpr (DIM == 3) {
-        A.z = group_sum<G>(A.z);
-        C.z = group_sum<G>(C.z);
-    }
-    {
+        // all lanes of the warp take part in the shuffles
+        rho = group_sum<G>(rho);
+        st = group_sum<G>(st);
+        A.x = group_sum<G>(A.x);
+        A.y = group_sum<G>(A.y);
+        C.x = group_sum<G>(C.x);
+        C.y = group_sum<G>(C.y);
+        if constexpr (DIM == 3) {
+            A.z = group_sum<G>(A.z);
+            C.z = group_sum<G>(C.z);
+        }
         if (valid && lg == 0) {
             float4 R = make_float4(0.f, 0.f, 0.f, 0.f);
             const int stride = DIM == 2 ? 2 : 4;
@@ -138,13 +141,14 @@ __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
             const bool fin = isfinite(xn.x) && isfinite(xn.y) && isfinite(xn.z);
             if (!fin) atomicOr(a.flags, 1);
             const double ex = (double)xn.x - xi.x, ey = (double)xn.y - xi.y, ez = (double)xn.z - xi.z;
-            v_dx2 = ex * ex + ey * ey + ez * ez;
-            v_x2 = (double)xi.x * xi.x + (double)xi.y * xi.y + (double)xi.z * xi.z;
-            v_st = (double)st;
+            v_dx2 += ex * ex + ey * ey + ez * ez;
+            v_x2 += (double)xi.x * xi.x + (double)xi.y * xi.y + (double)xi.z * xi.z;
+            v_st += (double)st;
         }
     }
     // fixed-order block reduction of (dx2, x2, stress)
     __shared__ double red[3][kGBlock / 32];
+    __shared__ bool last;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         v_dx2 += __shfl_xor_sync(0xffffffffu, v_dx2, o);
@@ -161,6 +165,40 @@ __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
         double s = 0.0;
         for (int w = 0; w < kGBlock / 32; ++w) s += red[threadIdx.x][w];
         a.stat_partial[(int64_t)blockIdx.x * 3 + threadIdx.x] = s;
+    }
+    // last CTA to finish reduces the per-CTA partials in CTA order (the order
+    // does not depend on which CTA is last) and re-arms the ticket and flags
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.ticket, 1) == (int)gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t[3] = {0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kGBlock)
+        for (int k = 0; k < 3; ++k) t[k] += __ldcg(a.stat_partial + (int64_t)b * 3 + k);
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t[k] += __shfl_xor_sync(0xffffffffu, t[k], o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 3; ++k) red[k][threadIdx.x >> 5] = t[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot[3] = {0.0, 0.0, 0.0};
+        for (int w = 0; w < kGBlock / 32; ++w)
+            for (int k = 0; k < 3; ++k) tot[k] += red[k][w];
+        const int32_t fl = atomicExch(a.flags, 0);
+        if (a.stats) {
+            a.stats->dx2 = tot[0];
+            a.stats->x2 = tot[1];
+            a.stats->stress = 0.5 * tot[2];
+            a.stats->flags = fl;
+            a.stats->pad = 0;
+        }
+        *a.ticket = 0;
     }
 }
 
@@ -265,7 +303,15 @@ int pick_group(double mean_row) {
 
 int gather_blocks(int32_t n, double mean_row) {
     const int G = pick_group(mean_row);
-    return (int)(((int64_t)n * G + kGBlock - 1) / kGBlock);
+    const int64_t need = ((int64_t)n * G + kGBlock - 1) / kGBlock;
+    static int cap = 0;
+    if (!cap) {
+        int dev = 0, sms = 148, occ = 6;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cap = sms * occ * 2;  // a few resident waves of grid-stride CTAs
+    }
+    return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
 }
 
 cudaError_t launch_gather(int dim, const GatherArgs& a, double mean_row, cudaStream_t st) {

@@ -34,42 +34,53 @@ __device__ __forceinline__ uint64_t match_hash(uint64_t seed, int32_t level, int
     return mix64(k ^ ((lo << 32) | hi));
 }
 
-// One thread per vertex: pick the best unmatched neighbour.
+// Candidate order of the handshake (Q16): higher rating omega/(c_u c_v)
+// (exact: w_a c_b vs w_b c_a in int64), then higher hash, then lower id.
+struct Cand {
+    int32_t v;
+    int32_t w;
+    int32_t c;
+    uint64_t h;
+};
+__device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
+    if (a.v < 0) return false;
+    if (b.v < 0) return true;
+    const int64_t lhs = (int64_t)a.w * b.c, rhs = (int64_t)b.w * a.c;
+    if (lhs != rhs) return lhs > rhs;
+    if (a.h != b.h) return a.h > b.h;
+    return a.v < b.v;
+}
+
+// One warp per vertex: lanes scan the row strided, then a shuffle reduction
+// under the (total) candidate order picks the best unmatched neighbour.
 __global__ void k_match_pick(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                              const int32_t* __restrict__ omega, const int32_t* __restrict__ c,
                              const int32_t* __restrict__ mate, int32_t* __restrict__ cand, uint64_t seed,
                              int32_t level, int32_t round) {
-    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
+    const int32_t u = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
+    if (u >= n) return;  // whole warp exits together
     if (mate[u] >= 0) {
-        cand[u] = -1;
+        if (lane == 0) cand[u] = -1;
         return;
     }
-    int32_t best = -1;
-    int64_t wb = 0, cb = 0;
-    uint64_t hb = 0;
-    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+    Cand best{-1, 0, 1, 0};
+    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
         const int32_t v = col[e];
         if (v == u || mate[v] >= 0) continue;
-        const int64_t wv = omega ? omega[e] : 1, cv = c[v];
-        const uint64_t hv = match_hash(seed, level, round, u, v);
-        bool better;
-        if (best < 0) {
-            better = true;
-        } else {
-            const int64_t lhs = wv * cb, rhs = wb * cv;  // wv/cv > wb/cb ?
-            if (lhs != rhs) better = lhs > rhs;
-            else if (hv != hb) better = hv > hb;
-            else better = v < best;
-        }
-        if (better) {
-            best = v;
-            wb = wv;
-            cb = cv;
-            hb = hv;
-        }
+        const Cand cv{v, omega ? omega[e] : 1, c[v], match_hash(seed, level, round, u, v)};
+        if (cand_better(cv, best)) best = cv;
     }
-    cand[u] = best;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        Cand other;
+        other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
+        other.w = __shfl_xor_sync(0xffffffffu, best.w, o);
+        other.c = __shfl_xor_sync(0xffffffffu, best.c, o);
+        other.h = __shfl_xor_sync(0xffffffffu, best.h, o);
+        if (cand_better(other, best)) best = other;
+    }
+    if (lane == 0) cand[u] = best.v;
 }
 
 __global__ void k_match_confirm(int32_t n, const int32_t* __restrict__ cand, int32_t* __restrict__ mate,
@@ -265,7 +276,7 @@ cudaError_t run_match_round(int32_t n, const int64_t* rp, const int32_t* col, co
                             int32_t round, int32_t* added, cudaStream_t st) {
     {
         LaunchScope ls("match_pick", st);
-        k_match_pick<<<nblk(n), 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round);
+        k_match_pick<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round);
     }
     {
         LaunchScope ls("match_confirm", st);

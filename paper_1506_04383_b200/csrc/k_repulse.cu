@@ -330,10 +330,14 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
     }
 }
 
+template <int DIM, bool QPOW, bool COARSE>
+constexpr int kBatchMask = (DIM == 2 && !QPOW && !COARSE) ? 1 : 0;
+
 template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_repulse<DIM, QPOW, COARSE, T>, kBlock, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>>,
+                                                  kBlock, 0);
     return occ > 0 ? occ : 1;
 }
 
@@ -386,8 +390,11 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
                            const RepulsePlan& p, float* part, cudaStream_t st) {
     const float cexp = -(q + 2.0f) * 0.5f;
     LaunchScope ls(coarse ? "repulse_coarse" : "repulse_exact", st);
+// batched reciprocals (BMASK) only where they pay: the exact 2-D q = 0 loop
+// (MUFU-bound); the coarse loop is FMA-bound already (hi/lo, nu), q > 0 has none.
 #define MM_LAUNCH(D, Q, C, T) \
-    k_repulse<D, Q, C, T><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, anc, cexp, p.sch, part)
+    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, anc, \
+                                                                          cexp, p.sch, part)
     if (dim == 2) {
         if (!qpow && !coarse) MM_LAUNCH(2, false, false, 4);
         else if (!qpow && coarse) MM_LAUNCH(2, false, true, 4);

@@ -67,7 +67,9 @@ struct GatherArgs {
     const int32_t* child;
     float* x_out;
     double* stat_partial; // [nblocks][3]
-    int32_t* flags;       // device int (OR-ed)
+    int32_t* flags;       // device int (OR-ed); re-armed to 0 by the last CTA
+    int32_t* ticket;      // device int, 0 between launches (last-CTA-done counter)
+    mm_sweep_stats* stats; // nullable: final fixed-order reduction target
 };
 int gather_blocks(int32_t n, double mean_row);
 cudaError_t launch_gather(int dim, const GatherArgs& a, double mean_row, cudaStream_t st);
