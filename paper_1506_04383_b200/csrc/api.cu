@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <map>
 #include <mutex>
 #include <string>
@@ -47,9 +48,26 @@ void* (*g_alloc)(size_t, mm_stream_t, void*) = nullptr;
 void (*g_free)(void*, mm_stream_t, void*) = nullptr;
 void* g_alloc_ctx = nullptr;
 
+// Keep freed blocks in the device's stream-ordered pool (the default release
+// threshold 0 returns them to the driver at every synchronisation, and the
+// next cudaMallocAsync would map fresh pages).
+void keep_pool_warm() {
+    static bool done = false;
+    if (done) return;
+    done = true;
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+}
+
 void* dev_alloc(size_t bytes, cudaStream_t st) {
     if (bytes == 0) bytes = 16;
     if (g_alloc) return g_alloc(bytes, (mm_stream_t)st, g_alloc_ctx);
+    keep_pool_warm();
     void* p = nullptr;
     if (cudaMallocAsync(&p, bytes, st) != cudaSuccess) {
         cudaGetLastError();
@@ -93,6 +111,22 @@ struct DevBuf {
     DevBuf& operator=(const DevBuf&) = delete;
 };
 
+// ------------------------------------------------------------------ host trace (MM_TRACE=1)
+bool trace_on() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MM_TRACE");
+        on = (e && e[0] && e[0] != '0') ? 1 : 0;
+    }
+    return on == 1;
+}
+void trace(const char* what) {
+    if (!trace_on()) return;
+    static auto t0 = std::chrono::steady_clock::now();
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    fprintf(stderr, "[mm_trace %12.1f us] %s\n", us, what);
+}
+
 // ------------------------------------------------------------------ profiling
 std::atomic<int64_t> g_launches{0};
 std::atomic<int> g_prof_on{0};
@@ -102,7 +136,19 @@ struct PendingEv {
     cudaEvent_t a, b;
 };
 std::vector<PendingEv> g_pending;
+std::vector<cudaEvent_t> g_event_pool;  // reused timing events (creation is not free)
 std::map<std::string, std::pair<int64_t, double>> g_prof;
+
+cudaEvent_t pool_get() {  // caller holds g_prof_mu
+    if (!g_event_pool.empty()) {
+        cudaEvent_t e = g_event_pool.back();
+        g_event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+}
 
 }  // namespace
 
@@ -112,10 +158,10 @@ LaunchScope::LaunchScope(const char* n, cudaStream_t s) : name(n), stream(s), sl
     if (!g_prof_on.load(std::memory_order_relaxed)) return;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return;
-    PendingEv ev{n, nullptr, nullptr};
-    if (cudaEventCreate(&ev.a) != cudaSuccess || cudaEventCreate(&ev.b) != cudaSuccess) return;
-    cudaEventRecord(ev.a, s);
     std::lock_guard<std::mutex> g(g_prof_mu);
+    PendingEv ev{n, pool_get(), pool_get()};
+    if (!ev.a || !ev.b) return;
+    cudaEventRecord(ev.a, s);
     g_pending.push_back(ev);
     slot = (int)g_pending.size() - 1;
 }
@@ -433,8 +479,8 @@ mm_status mm_profile_reset(void) {
     std::lock_guard<std::mutex> g(g_prof_mu);
     for (auto& p : g_pending) {
         cudaEventSynchronize(p.b);
-        cudaEventDestroy(p.a);
-        cudaEventDestroy(p.b);
+        g_event_pool.push_back(p.a);
+        g_event_pool.push_back(p.b);
     }
     g_pending.clear();
     g_prof.clear();
@@ -453,8 +499,8 @@ mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count) {
         } else {
             cudaGetLastError();
         }
-        cudaEventDestroy(p.a);
-        cudaEventDestroy(p.b);
+        g_event_pool.push_back(p.a);
+        g_event_pool.push_back(p.b);
     }
     g_pending.clear();
     int32_t i = 0;
@@ -913,6 +959,7 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
 
     mm_layout_report R;
     memset(&R, 0, sizeof(R));
+    trace("layout: begin");
     const auto K_of = [&](int32_t l) { return sweeps[std::min(l, nsweeps - 1)]; };
 
     if (h == 0) {
@@ -945,11 +992,14 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
             B = (A == x_out) ? tmpx : x_out;
         }
         const float* res = nullptr;
+        trace("layout: sweeps enqueue");
         MM_CU(run_sweeps(S, dim, alpha, q, nullptr, src, A, B, K, dstats, sb, ls, &res), "mm_layout sweeps");
+        trace("layout: sweeps enqueued");
         if (res != x_out) MM_CU(cudaMemcpyAsync(x_out, res, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
         mm_sweep_stats hs;
         MM_CU(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, ls), "mm_layout d2h");
         MM_CU(cudaStreamSynchronize(ls), "mm_layout sync");
+        trace("layout: sweeps done (synced)");
         R.levels = 1;
         R.n_level[0] = n0;
         R.rel_change = hs.x2 > 0 ? sqrt(hs.dx2 / hs.x2) : INFINITY;
@@ -1052,7 +1102,9 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
     }
     double en[3] = {0, 0, 0};
     int64_t coinc = 0;
+    trace("layout: energy begin");
     s = energy_core(S, dim, alpha, q, x_out, en, ls, false, &coinc);
+    trace("layout: energy done");
     R.coincident_pairs = coinc;
     R.stress = en[0];
     R.entropy = en[1];

@@ -65,9 +65,25 @@ __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
         float4 xi = make_float4(0.f, 0.f, 0.f, 0.f);
         float rho = 0.f, st = 0.f;
         float4 A = make_float4(0.f, 0.f, 0.f, 0.f), C = A;
+        float4 R = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
             xi = load_x<DIM>(a.x, i);
+            if (lg == 0) {
+                // repulsion partials of this vertex (static schedule slots), fetched
+                // first so that their latency overlaps the S-row loads
+                const int stride = DIM == 2 ? 2 : 4;
+                const int64_t tb = i / a.tpb;
+                const int32_t nslot = sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
+                                      sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
+                for (int p = 0; p < nslot; ++p) {
+                    const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
+                    R.x += v.x;
+                    R.y += v.y;
+                    R.z += v.z;
+                }
+            }
             const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];
+#pragma unroll 2
             for (int64_t e = e0 + lg; e < e1; e += G) {
                 const int32_t j = __ldg(a.col + e);
                 const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);
@@ -117,18 +133,6 @@ __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
             C.z = group_sum<G>(C.z);
         }
         if (valid && lg == 0) {
-            float4 R = make_float4(0.f, 0.f, 0.f, 0.f);
-            const int stride = DIM == 2 ? 2 : 4;
-            // partial slots written for this vertex's target block (static schedule)
-            const int64_t tb = i / a.tpb;
-            const int32_t nslot = sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
-                                  sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
-            for (int p = 0; p < nslot; ++p) {
-                const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
-                R.x += v.x;
-                R.y += v.y;
-                R.z += v.z;
-            }
             R.x -= C.x;
             R.y -= C.y;
             R.z -= C.z;
@@ -236,10 +240,13 @@ __global__ void __launch_bounds__(kGBlock) k_energy_s(int32_t n, const int64_t* 
                                                       float cq, double* __restrict__ partial,
                                                       int32_t* __restrict__ coinc) {
     const int lg = threadIdx.x & (G - 1);
-    const int64_t i = ((int64_t)blockIdx.x * kGBlock + threadIdx.x) / G;
-    float st = 0.f, ph = 0.f;
+    constexpr int VPB = kGBlock / G;
+    double a0 = 0.0, a1 = 0.0;  // FP64 across vertices, FP32 within a row
     int32_t zc = 0;
-    if (i < n) {
+    for (int64_t vb = (int64_t)blockIdx.x * VPB; vb < n; vb += (int64_t)gridDim.x * VPB) {
+        const int64_t i = vb + threadIdx.x / G;
+        if (i >= n) continue;
+        float st = 0.f, ph = 0.f;
         const float4 xi = load_x<DIM>(x, i);
         for (int64_t e = rp[i] + lg; e < rp[i + 1]; e += G) {
             const float4 xj = load_x<DIM>(x, __ldg(col + e));
@@ -262,8 +269,9 @@ __global__ void __launch_bounds__(kGBlock) k_energy_s(int32_t n, const int64_t* 
                 else ph += ex2_approx(fminf(cq * l, kExpClamp));
             }
         }
+        a0 += (double)st;
+        a1 += (double)ph;
     }
-    double a0 = st, a1 = ph;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         a0 += __shfl_xor_sync(0xffffffffu, a0, o);
@@ -293,6 +301,12 @@ __global__ void __launch_bounds__(kGBlock) k_energy_s(int32_t n, const int64_t* 
 }
 
 int pick_group(double mean_row) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("MM_GATHER_G");  // experiments: 1, 2, 4, 8, 16, 32
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     if (mean_row >= 32) return 32;
     if (mean_row >= 16) return 16;
     if (mean_row >= 8) return 8;
@@ -322,6 +336,8 @@ cudaError_t launch_gather(int dim, const GatherArgs& a, double mean_row, cudaStr
     LaunchScope ls("gather_update", st);
 #define MM_G(D, Q)                                                                  \
     switch (G) {                                                                    \
+        case 1: k_gather<D, Q, 1><<<nb, kGBlock, 0, st>>>(a, cexp); break;          \
+        case 2: k_gather<D, Q, 2><<<nb, kGBlock, 0, st>>>(a, cexp); break;          \
         case 4: k_gather<D, Q, 4><<<nb, kGBlock, 0, st>>>(a, cexp); break;          \
         case 8: k_gather<D, Q, 8><<<nb, kGBlock, 0, st>>>(a, cexp); break;          \
         case 16: k_gather<D, Q, 16><<<nb, kGBlock, 0, st>>>(a, cexp); break;        \
@@ -353,6 +369,8 @@ cudaError_t launch_energy_s(int dim, double q, int32_t n, const int64_t* rp, con
     LaunchScope ls("energy_s", st);
 #define MM_E(D, Q)                                                                                  \
     switch (G) {                                                                                    \
+        case 1: k_energy_s<D, Q, 1><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break;   \
+        case 2: k_energy_s<D, Q, 2><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break;   \
         case 4: k_energy_s<D, Q, 4><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break;   \
         case 8: k_energy_s<D, Q, 8><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break;   \
         case 16: k_energy_s<D, Q, 16><<<nb, kGBlock, 0, st>>>(n, rp, col, d, w, x, cq, partial, coinc); break; \

@@ -331,14 +331,18 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
 }
 
 template <int DIM, bool QPOW, bool COARSE>
-constexpr int kBatchMask = (DIM == 2 && !QPOW && !COARSE) ? 1 : 0;
+constexpr int kBatchMask = (DIM == 2 && !QPOW) ? 1 : 0;  // measured: tools/ubench_repulse.cu
 
 template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>>,
-                                                  kBlock, 0);
-    return occ > 0 ? occ : 1;
+    static int occ = 0;  // per instantiation; queried once
+    if (!occ) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>>,
+                                                      kBlock, 0);
+        occ = o > 0 ? o : 1;
+    }
+    return occ;
 }
 
 int sm_count() {
@@ -390,8 +394,8 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
                            const RepulsePlan& p, float* part, cudaStream_t st) {
     const float cexp = -(q + 2.0f) * 0.5f;
     LaunchScope ls(coarse ? "repulse_coarse" : "repulse_exact", st);
-// batched reciprocals (BMASK) only where they pay: the exact 2-D q = 0 loop
-// (MUFU-bound); the coarse loop is FMA-bound already (hi/lo, nu), q > 0 has none.
+// batched reciprocals (BMASK) in half of the target groups for 2-D q = 0
+// (exact and coarse: measured faster by tools/ubench_repulse.cu); none for q > 0.
 #define MM_LAUNCH(D, Q, C, T) \
     k_repulse<D, Q, C, T, kBatchMask<D, Q, C>><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, anc, \
                                                                           cexp, p.sch, part)
@@ -420,9 +424,13 @@ EntropyPlan plan_entropy(int32_t n) {
     t.Ub = (int32_t)((n + kBlock - 1) / kBlock);
     t.c = TPB / kBlock;
     t.U = tri_prefix(t.TB, t);
-    int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_entropy_tri<2, false>, kBlock, 0);
-    t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * std::max(occ, 1), t.U));
+    static int occ = 0;
+    if (!occ) {
+        int o = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_entropy_tri<2, false>, kBlock, 0);
+        occ = std::max(o, 1);
+    }
+    t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * occ, t.U));
     p.nblocks = t.G;
     return p;
 }
