@@ -307,10 +307,11 @@ int pick_group(double mean_row) {
         forced = e ? atoi(e) : 0;
     }
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
-    if (mean_row >= 32) return 32;
-    if (mean_row >= 16) return 16;
-    if (mean_row >= 8) return 8;
-    return 4;
+    // about 8 row entries per lane: more independent loads in flight per lane
+    // beat wider groups (tools/bench_gather.py sweep, profiles/r01_gather_groups.txt)
+    int g = 1;
+    while (g < 32 && 8.0 * (2 * g) <= mean_row) g *= 2;
+    return g;
 }
 
 }  // namespace
