@@ -52,8 +52,15 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
     if constexpr (DIM == 3) acc.z = fmaf(dz, inv, acc.z);
 }
 
+#ifndef MM_GATHER_MINB
+#define MM_GATHER_MINB 1
+#endif
+#ifndef MM_GATHER_UNROLL
+#define MM_GATHER_UNROLL 2
+#endif
+constexpr int kGatherUnroll = MM_GATHER_UNROLL;
 template <int DIM, bool QPOW, int G>
-__global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
+__global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a, float cexp) {
     const int lg = threadIdx.x & (G - 1);
     constexpr int VPB = kGBlock / G;  // vertices per block iteration
     double v_dx2 = 0.0, v_x2 = 0.0, v_st = 0.0;
@@ -83,7 +90,7 @@ __global__ void __launch_bounds__(kGBlock) k_gather(GatherArgs a, float cexp) {
                 }
             }
             const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];
-#pragma unroll 2
+#pragma unroll kGatherUnroll
             for (int64_t e = e0 + lg; e < e1; e += G) {
                 const int32_t j = __ldg(a.col + e);
                 const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);

@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmm_b200.so")
+LIB_PATH = os.environ.get("MM_LIB_PATH") or os.path.join(_HERE, "libmm_b200.so")  # override: experiments only
 
 MM_OK, MM_ERR_INVALID_ARGUMENT, MM_ERR_INVALID_INPUT, MM_ERR_NONFINITE = 0, -1, -2, -3
 MM_ERR_OUT_OF_MEMORY, MM_ERR_CUDA, MM_ERR_UNSUPPORTED = -4, -5, -6
