@@ -53,10 +53,10 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
 }
 
 #ifndef MM_GATHER_MINB
-#define MM_GATHER_MINB 1
+#define MM_GATHER_MINB 4
 #endif
 #ifndef MM_GATHER_UNROLL
-#define MM_GATHER_UNROLL 2
+#define MM_GATHER_UNROLL 4
 #endif
 constexpr int kGatherUnroll = MM_GATHER_UNROLL;
 template <int DIM, bool QPOW, int G>
