@@ -676,10 +676,6 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
                 return fail(MM_ERR_CUDA);
             }
             m2 = (int64_t)lastp[0] + lastp[1];
-        } else if (launch_fill(nc + 1, 0, rowcnt, st) != cudaSuccess) {
-            dev_free(parent, st);
-            set_err("mm_build_hierarchy: fill failed");
-            return fail(MM_ERR_CUDA);
         }
         HLevel nx;
         nx.n = nc;
@@ -696,7 +692,7 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
             set_err("mm_build_hierarchy: out of memory");
             return fail(MM_ERR_OUT_OF_MEMORY);
         }
-        if (rowptr_from_counts(nc, rowcnt, excl, m2, nx.rp, tmp, tmpb, st) ||
+        if (rowptr_from_rows(nc, vals, m2, nx.rp, st) ||
             (m2 > 0 && cudaMemcpyAsync(nx.col, ccol, 4 * m2, cudaMemcpyDeviceToDevice, st)) ||
             (m2 > 0 && cudaMemcpyAsync(nx.omega, comega, 4 * m2, cudaMemcpyDeviceToDevice, st)) ||
             cudaMemcpyAsync(nx.c, cnext, 4 * (size_t)nc, cudaMemcpyDeviceToDevice, st) ||

@@ -118,13 +118,15 @@ __global__ void k_parent(int32_t n, const int32_t* __restrict__ mate, const int3
 }
 
 // keys (parent[u] * nc + parent[v]) for crossing entries; intra-cluster -> sentinel nc*nc
+// (one warp per row: coarse Chung-Lu levels have rows of 10^4-10^5 entries)
 __global__ void k_edge_keys(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                             const int32_t* __restrict__ omega, const int32_t* __restrict__ parent, int64_t nc,
                             uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
-    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t u = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int lane = threadIdx.x & 31;
     if (u >= n) return;
     const int64_t pu = parent[u];
-    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
         const int64_t pv = parent[col[e]];
         keys[e] = (pu != pv) ? (uint64_t)(pu * nc + pv) : (uint64_t)(nc * nc);
         vals[e] = omega ? omega[e] : 1;
@@ -138,10 +140,10 @@ __global__ void k_run_heads(int64_t m, const uint64_t* __restrict__ keys, uint64
     head[t] = (k != sentinel && (t == 0 || keys[t - 1] != k)) ? 1 : 0;
 }
 
-// for each run head: write coarse col / omega (sum over the run) and count the row
+// for each run head: write coarse col / omega (sum over the run) and the row id
 __global__ void k_run_emit(int64_t m, const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals,
                            const int32_t* __restrict__ head, const int32_t* __restrict__ pos, int64_t nc,
-                           int32_t* __restrict__ ccol, int32_t* __restrict__ comega, int32_t* __restrict__ rowcnt) {
+                           int32_t* __restrict__ ccol, int32_t* __restrict__ comega, int32_t* __restrict__ urow) {
     const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= m || !head[t]) return;
     const uint64_t k = keys[t];
@@ -150,22 +152,28 @@ __global__ void k_run_emit(int64_t m, const uint64_t* __restrict__ keys, const i
     const int32_t p = pos[t];
     ccol[p] = (int32_t)(k % (uint64_t)nc);
     comega[p] = s;
-    atomicAdd(rowcnt + (k / (uint64_t)nc), 1);
+    urow[p] = (int32_t)(k / (uint64_t)nc);
 }
 
-__global__ void k_i32_to_i64_rowptr(int32_t n, const int32_t* __restrict__ excl, int64_t total,
-                                    int64_t* __restrict__ rp) {
-    const int32_t t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t < n) rp[t] = excl[t];
-    if (t == n) rp[n] = total;
+// row_ptr[p] = first unique entry with row >= p (binary search; no atomics)
+__global__ void k_rowptr_search(int32_t nc, const int32_t* __restrict__ urow, int64_t m2, int64_t* __restrict__ rp) {
+    const int32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > nc) return;
+    int64_t lo = 0, hi = m2;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (urow[mid] < p) lo = mid + 1; else hi = mid;
+    }
+    rp[p] = lo;
 }
 
 __global__ void k_coarse_sset(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                               const int32_t* __restrict__ c, int dim, float* __restrict__ d, float* __restrict__ w) {
-    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t u = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // warp per row
+    const int lane = threadIdx.x & 31;
     if (u >= n) return;
     const float su = dim == 2 ? sqrtf((float)c[u]) : cbrtf((float)c[u]);
-    for (int64_t e = rp[u]; e < rp[u + 1]; ++e) {
+    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
         const int32_t v = col[e];
         const float sv = dim == 2 ? sqrtf((float)c[v]) : cbrtf((float)c[v]);
         const float dd = su + sv;
@@ -338,7 +346,7 @@ cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int3
     cudaError_t e;
     {
         LaunchScope ls("edge_keys", st);
-        k_edge_keys<<<nblk(n), 256, 0, st>>>(n, rp, col, omega, parent, nc, keys, vals);
+        k_edge_keys<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, col, omega, parent, nc, keys, vals);
     }
     const uint64_t sentinel = (uint64_t)nc * (uint64_t)nc;
     int end_bit = 1;
@@ -354,26 +362,23 @@ cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int3
     }
     e = exclusive_scan_i32(head, pos, (int32_t)nnz, tmp, tmp_bytes, st);
     if (e != cudaSuccess) return e;
-    e = launch_fill(nc + 1, 0, rowcnt, st);
-    if (e != cudaSuccess) return e;
+    (void)rowcnt;
     LaunchScope ls("run_emit", st);
-    k_run_emit<<<nblk(nnz), 256, 0, st>>>(nnz, keys_alt, vals_alt, head, pos, nc, ccol_tmp, comega_tmp, rowcnt);
+    // vals (pre-sort values) is dead after the sort: reuse it for the row ids
+    k_run_emit<<<nblk(nnz), 256, 0, st>>>(nnz, keys_alt, vals_alt, head, pos, nc, ccol_tmp, comega_tmp, vals);
     return cudaGetLastError();
 }
 
-cudaError_t rowptr_from_counts(int32_t nc, const int32_t* rowcnt, int32_t* excl, int64_t total, int64_t* rp,
-                               void* tmp, size_t tmp_bytes, cudaStream_t st) {
-    cudaError_t e = exclusive_scan_i32(rowcnt, excl, nc, tmp, tmp_bytes, st);
-    if (e != cudaSuccess) return e;
+cudaError_t rowptr_from_rows(int32_t nc, const int32_t* urow, int64_t m2, int64_t* rp, cudaStream_t st) {
     LaunchScope ls("rowptr", st);
-    k_i32_to_i64_rowptr<<<nblk(nc + 1), 256, 0, st>>>(nc, excl, total, rp);
+    k_rowptr_search<<<nblk((int64_t)nc + 1), 256, 0, st>>>(nc, urow, m2, rp);
     return cudaGetLastError();
 }
 
 cudaError_t launch_coarse_sset(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* c, int dim,
                                float* d, float* w, cudaStream_t st) {
     LaunchScope ls("coarse_sset", st);
-    k_coarse_sset<<<nblk(n), 256, 0, st>>>(n, rp, col, c, dim, d, w);
+    k_coarse_sset<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, col, c, dim, d, w);
     return cudaGetLastError();
 }
 

@@ -19,8 +19,8 @@ cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int3
                            const int32_t* parent, int32_t nc, uint64_t* keys, uint64_t* keys_alt, int32_t* vals,
                            int32_t* vals_alt, int32_t* head, int32_t* pos, int32_t* ccol_tmp,
                            int32_t* comega_tmp, int32_t* rowcnt, void* tmp, size_t tmp_bytes, cudaStream_t st);
-cudaError_t rowptr_from_counts(int32_t nc, const int32_t* rowcnt, int32_t* excl, int64_t total, int64_t* rp,
-                               void* tmp, size_t tmp_bytes, cudaStream_t st);
+// coarse row_ptr from the row ids of the m2 unique entries (written into `vals` by contract_edges)
+cudaError_t rowptr_from_rows(int32_t nc, const int32_t* urow, int64_t m2, int64_t* rp, cudaStream_t st);
 cudaError_t launch_coarse_sset(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* c, int dim,
                                float* d, float* w, cudaStream_t st);
 cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr, int32_t* members,
