@@ -126,7 +126,18 @@ typedef struct {
     int64_t pair_interactions;          /* repulsion pairs evaluated (DESIGN.md §5 convention) */
     int64_t coincident_pairs;           /* non-S ordered pairs at distance exactly 0 in the final
                                            layout; they are left out of `entropy` (ln 0 undefined) */
+    int32_t sweeps_level[MM_MAX_LEVELS]; /* Jacobi sweeps performed at level l */
 } mm_layout_report;
+
+/* The paper's optimizer schedule: alpha0 = 1,
+ * factor = 0.3, alpha_min = 0.008, a = 2 iterations per round, eps = 1e-4;
+ * max_final_iters caps the alpha_min phase (not in the paper). */
+typedef struct {
+    double alpha0, alpha_min, factor, eps;
+    int32_t a, max_final_iters;
+} mm_schedule;
+#define MM_LAYOUT_MULTILEVEL 1 /* hierarchy + prolongation; h = 0: exact Eq.(2) on every level */
+#define MM_LAYOUT_DYNAMIC 2    /* dynamic update: finest level only, from x_init, at alpha_min */
 
 /* ------------------------------------------------------------------ API */
 
@@ -203,6 +214,24 @@ MM_API mm_status mm_hierarchy_copy_level(const mm_hierarchy* h, int32_t level, i
 MM_API mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, float alpha, float q, int h,
                     const int32_t* sweeps, int32_t nsweeps, uint64_t seed, int32_t n_stop,
                     const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream);
+
+/* Layout with the paper's schedule instead of fixed alpha / sweep counts.
+ * Per optimized level (R1: the schedule restarts on every level): rounds at
+ * alpha = alpha0, factor*alpha, ... clamped to alpha_min (R2), each of at most
+ * `a` sweeps and cut short once the relative change |x'-x|/|x| < eps; at
+ * alpha_min sweeps continue until the relative change < eps or max_final_iters
+ * (R3).  flags = 0: one level from x_init (exact Eq.(2)).  MM_LAYOUT_MULTILEVEL:
+ * hierarchy (n_stop, seed), box init of the coarsest level, prolongation, exact
+ * sweeps when h = 0, else Eq.(3) with h' = min(h, L-l).  MM_LAYOUT_DYNAMIC: the
+ * paper's update algorithm — hierarchy stopped after h levels, only the finest
+ * level is optimized, from x_init (device, required), starting at alpha_min;
+ * the representatives are the cluster midpoints of the current layout.
+ * The report's energy is Eq.(1) at alpha_min (the paper's final penalty level,
+ * P:324); rep->sweeps_level holds the sweeps run per level.  Syncs (once per
+ * sweep: each schedule decision reads the sweep's relative change). */
+MM_API mm_status mm_layout_schedule(const mm_graph* g, const mm_sset* S, int dim, float q, int h,
+                                    const mm_schedule* sch, uint64_t seed, int32_t n_stop, int32_t flags,
+                                    const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream);
 
 /* ------------------------------------------------------------------ instrumentation */
 /* Total kernels launched by this library since load (host counter). */

@@ -30,7 +30,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["rng.c", "sweep.c", "energy.c", "hierarchy.c", "layout.c"]
+_SRCS = ["rng.c", "sweep.c", "energy.c", "hierarchy.c", "layout.c", "schedule.c"]
 
 OR_EINVAL, OR_ERHO, OR_ECOINC, OR_ENOMEM = -1, -2, -3, -4
 TAG_INIT, TAG_JITTER, TAG_MATCH = 0x494E4954, 0x4A495454, 0x4D415443
@@ -53,6 +53,18 @@ def build(force: bool = False) -> str:
            "-shared", "-fPIC", "-o", _LIB_PATH] + [os.path.join(_HERE, s) for s in _SRCS] + ["-lm"]
     subprocess.check_call(cmd)
     return _LIB_PATH
+
+
+class Schedule(ctypes.Structure):
+    """or_schedule: the paper's defaults; max_final_iters is a safety cap."""
+    _fields_ = [("alpha0", ctypes.c_double), ("alpha_min", ctypes.c_double), ("factor", ctypes.c_double),
+                ("eps", ctypes.c_double), ("a", ctypes.c_int32), ("max_final_iters", ctypes.c_int32)]
+
+
+def paper_schedule(**kw) -> Schedule:
+    v = dict(alpha0=1.0, alpha_min=0.008, factor=0.3, eps=1e-4, a=2, max_final_iters=200)
+    v.update(kw)
+    return Schedule(**v)
 
 
 _lib = None
@@ -90,6 +102,9 @@ def lib() -> ctypes.CDLL:
     L.or_prolong.argtypes = [c_i32, c_int, _i32p, _f64p, c_u64, c_i32, _f64p]
     L.or_layout.argtypes = [c_i32, c_int, _i64p, _i32p, _i64p, _i32p, _f64p, _f64p, c_dbl, c_dbl, c_int,
                             _i32p, c_i32, c_u64, c_i32, _f64p, _f64p, _f64p, _i32p, c_int]
+    L.or_layout_schedule.argtypes = [c_i32, c_int, _i64p, _i32p, _i64p, _i32p, _f64p, _f64p, c_dbl, c_int,
+                                     ctypes.POINTER(Schedule), c_u64, c_i32, c_int, _f64p, _f64p, _f64p, _i32p, _i32p,
+                                     c_int]
     _lib = L
     return L
 
@@ -308,3 +323,26 @@ def layout(g, S, dim: int, alpha: float, q: float, h: int, sweeps, seed: int, n_
                            _p(out, ctypes.c_double), _p(en, ctypes.c_double), ctypes.byref(nl),
                            nthreads or default_threads()), "layout")
     return out, (float(en[0]), float(en[1]), float(en[2])), nl.value
+
+
+def layout_schedule(g, S, dim: int, q: float, h: int, sched: Schedule, seed: int, n_stop: int = 1000,
+                    multilevel: bool = True, dynamic: bool = False, x_init: Optional[np.ndarray] = None,
+                    nthreads: Optional[int] = None):
+    """The paper's schedule or the dynamic update.
+    Returns (x0, (stress, entropy, total at alpha_min), levels, sweeps per level)."""
+    rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(g.col, dtype=np.int32)
+    srp, scol, d, w = _csr(S)
+    xi = None if x_init is None else np.ascontiguousarray(x_init, dtype=np.float64)
+    n = g.n
+    out = np.empty((n, dim), dtype=np.float64)
+    en = np.zeros(3, dtype=np.float64)
+    nl = ctypes.c_int32()
+    sw = np.zeros(64, dtype=np.int32)
+    flags = (1 if multilevel else 0) | (2 if dynamic else 0)
+    _check(lib().or_layout_schedule(n, dim, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(srp, ctypes.c_int64),
+                                    _p(scol, ctypes.c_int32), _p(d, ctypes.c_double), _p(w, ctypes.c_double), q, h,
+                                    ctypes.byref(sched), seed, n_stop, flags, _p(xi, ctypes.c_double),
+                                    _p(out, ctypes.c_double), _p(en, ctypes.c_double), ctypes.byref(nl),
+                                    _p(sw, ctypes.c_int32), nthreads or default_threads()), "layout_schedule")
+    return out, (float(en[0]), float(en[1]), float(en[2])), nl.value, sw[:nl.value].copy()

@@ -100,6 +100,27 @@ int or_layout(int32_t n, int dim, const int64_t* rp, const int32_t* col,
               uint64_t seed, int32_t n_stop, const double* x_init, double* out,
               double energy_out[3], int32_t* levels_out, int nthreads);
 
+/* ---- the paper's optimizer schedule, reading R1-R4
+ * of DESIGN.md §3: per level, alpha starts at alpha0; a round runs at most
+ * `a` Jacobi sweeps at one alpha and ends early when the relative change
+ * |x' - x| / |x| < eps; then alpha <- max(factor * alpha, alpha_min).  At
+ * alpha_min, sweeps continue until the relative change < eps or
+ * max_final_iters sweeps.  flags bit 0: multilevel (hierarchy + prolongation;
+ * exact Eq.(2) everywhere when h = 0, Eq.(3) with h' = min(h, L - l) otherwise),
+ * else one level from x_init.  flags bit 1: dynamic update: start
+ * at alpha_min on the finest level only, from x_init, with the hierarchy built
+ * to at most h levels above the finest (the approximation level).
+ * sweeps_out[l] = sweeps performed at level l (nullable, 64 entries). */
+typedef struct {
+    double alpha0, alpha_min, factor, eps;
+    int32_t a, max_final_iters;
+} or_schedule;
+int or_layout_schedule(int32_t n, int dim, const int64_t* rp, const int32_t* col,
+                       const int64_t* srp, const int32_t* scol, const double* d, const double* w,
+                       double q, int h, const or_schedule* sch, uint64_t seed, int32_t n_stop, int flags,
+                       const double* x_init, double* out, double energy_out[3], int32_t* levels_out,
+                       int32_t* sweeps_out, int nthreads);
+
 #define OR_TAG_INIT 0x494e4954ULL   /* "INIT" */
 #define OR_TAG_JITTER 0x4a495454ULL /* "JITT" */
 #define OR_TAG_MATCH 0x4d415443ULL  /* "MATC" */

@@ -909,29 +909,87 @@ cudaError_t run_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm
 
 }  // namespace
 
-extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, float alpha, float q, int h,
-                               const int32_t* sweeps, int32_t nsweeps, uint64_t seed, int32_t n_stop,
-                               const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream) {
+namespace {
+
+// ------------------------------------------------------------------ per-level runners
+// A runner performs the sweeps of one level, starting from `src` (read-only
+// until consumed) and ping-ponging between A and B; it returns the buffer
+// holding the result and the number of sweeps it ran.
+struct Runner {
+    virtual ~Runner() {}
+    virtual mm_status run(const mm_sset* S, int dim, float q, const mm_approx* ap, const float* src, float* A, float* B,
+                          mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int32_t level,
+                          bool start_at_min, const float** res, int32_t* sweeps) = 0;
+};
+
+// Fixed alpha and sweep counts (BASELINE.json configs): the K sweeps of a
+// level are one cached CUDA graph.
+struct FixedRunner : Runner {
+    float alpha;
+    const int32_t* sweeps;
+    int32_t nsweeps;
+    mm_status run(const mm_sset* S, int dim, float q, const mm_approx* ap, const float* src, float* A, float* B,
+                  mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int32_t level, bool,
+                  const float** res, int32_t* nsw) override {
+        const int32_t K = sweeps[std::min(level, nsweeps - 1)];
+        MM_CU(run_sweeps(S, dim, alpha, q, ap, src, A, B, K, dstats, sb, ls, res), "mm_layout sweeps");
+        *nsw = K;
+        return MM_OK;
+    }
+};
+
+// The paper's schedule (readings R1-R4): rounds of at
+// most `a` sweeps per alpha, cut short when the relative change < eps, alpha
+// <- max(factor alpha, alpha_min); at alpha_min until converged (or the cap).
+// Each decision needs the relative change of the sweep just run: the fused
+// stats are read back after every sweep (one small D2H + sync per sweep).
+struct ScheduleRunner : Runner {
+    mm_schedule sch;
+    mm_status run(const mm_sset* S, int dim, float q, const mm_approx* ap, const float* src, float* A, float* B,
+                  mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int32_t, bool start_at_min,
+                  const float** res, int32_t* nsw) override {
+        double alpha = start_at_min ? sch.alpha_min : sch.alpha0;
+        const float* cur = src;
+        int32_t count = 0;
+        mm_sweep_stats hs;
+        for (;;) {
+            const bool final = alpha <= sch.alpha_min;
+            const int32_t max_it = final ? sch.max_final_iters : sch.a;
+            for (int32_t it = 0; it < max_it; ++it) {
+                float* dst = (cur == A) ? B : A;
+                MM_CU(sweep_core(S, dim, (float)alpha, q, ap, cur, dst, dstats, sb, ls), "mm_layout_schedule sweep");
+                MM_CU(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, ls), "mm_layout_schedule d2h");
+                MM_CU(cudaStreamSynchronize(ls), "mm_layout_schedule sync");
+                cur = dst;
+                ++count;
+                if (hs.flags & 1) {
+                    set_err("mm_layout_schedule: non-finite coordinate produced");
+                    return MM_ERR_NONFINITE;
+                }
+                const double rel = hs.x2 > 0 ? sqrt(hs.dx2) / sqrt(hs.x2) : INFINITY;
+                if (rel < sch.eps) break;
+            }
+            if (final) break;
+            alpha = std::max(alpha * sch.factor, sch.alpha_min);
+        }
+        *res = cur;
+        *nsw = count;
+        return MM_OK;
+    }
+};
+
+// Shared multilevel / single-level driver of mm_layout and mm_layout_schedule.
+// flags: MM_LAYOUT_MULTILEVEL (hierarchy + prolongation, exact when h = 0,
+// Eq.(3) with h' = min(h, L - l) otherwise), MM_LAYOUT_DYNAMIC (finest level
+// only, from x_init, starting at alpha_min, hierarchy stopped after h levels).
+mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int h, Runner& run, double alpha_energy,
+                      uint64_t seed, int32_t n_stop, int flags, const float* x_init, float* x_out,
+                      mm_layout_report* rep, cudaStream_t us, const char* who) {
     mm_status s;
-    if ((s = check_sset(S, "mm_layout")) != MM_OK) return s;
-    if ((s = check_dim_q(dim, q, "mm_layout")) != MM_OK) return s;
-    if ((s = check_x(x_out, dim, "x_out", "mm_layout")) != MM_OK) return s;
-    if (!sweeps || nsweeps < 1 || h < 0 || !isfinite(alpha)) {
-        set_err("mm_layout: bad arguments (sweeps host array with nsweeps >= 1, h >= 0, finite alpha)");
-        return MM_ERR_INVALID_ARGUMENT;
-    }
-    for (int32_t t = 0; t < nsweeps; ++t)
-        if (sweeps[t] < 0) { set_err("mm_layout: negative sweep count"); return MM_ERR_INVALID_ARGUMENT; }
-    if (h == 0 && (s = check_x(x_init, dim, "x_init", "mm_layout")) != MM_OK) return s;
-    if (h > 0) {
-        if ((s = check_graph(g, "mm_layout")) != MM_OK) return s;
-        if (g->n != S->n) { set_err("mm_layout: graph and S sizes differ"); return MM_ERR_INVALID_ARGUMENT; }
-        if (n_stop < 1) { set_err("mm_layout: n_stop must be >= 1"); return MM_ERR_INVALID_ARGUMENT; }
-    }
+    const bool multilevel = (flags & MM_LAYOUT_MULTILEVEL) != 0, dynamic = (flags & MM_LAYOUT_DYNAMIC) != 0;
     const int32_t n0 = S->n;
     const int st_w = stride_of(dim);
     const size_t xbytes = (size_t)n0 * st_w * sizeof(float);
-    cudaStream_t us = (cudaStream_t)stream;
     cudaEvent_t ev = nullptr;
     // the driver's own non-blocking stream (persistent, so that stream-ordered
     // workspace reuse and the graph cache see the same addresses call after call)
@@ -956,40 +1014,33 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
     mm_layout_report R;
     memset(&R, 0, sizeof(R));
     trace("layout: begin");
-    const auto K_of = [&](int32_t l) { return sweeps[std::min(l, nsweeps - 1)]; };
 
-    if (h == 0) {
-        const int32_t K = K_of(0);
+    if (!multilevel && !dynamic) {
         const double mean_row = (double)S->nnz / n0;
         const size_t need = sweep_bytes(n0, dim, 0, false, mean_row) + al(xbytes) + al(sizeof(mm_sweep_stats));
         DevBuf buf(need, ls);
-        if (!buf.p) { set_err("mm_layout: out of device memory (%zu B)", need); return MM_ERR_OUT_OF_MEMORY; }
+        if (!buf.p) { set_err("%s: out of device memory (%zu B)", who, need); return MM_ERR_OUT_OF_MEMORY; }
         Carver cv(buf.p, need);
         float* tmpx = cv.take<float>((size_t)n0 * st_w);
         mm_sweep_stats* dstats = cv.take<mm_sweep_stats>(1);
         SweepBufs sb;
-        if (!carve_sweep(cv, n0, dim, 0, false, mean_row, sb)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
+        if (!carve_sweep(cv, n0, dim, 0, false, mean_row, sb)) { set_err("%s: carving failed", who); return MM_ERR_INVALID_ARGUMENT; }
         MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
         MM_CU(cudaMemsetAsync(dstats, 0, sizeof(mm_sweep_stats), ls), "mm_layout memset");
-        // choose the first destination so that the last sweep lands in x_out
         const float* src = x_init;
-        float *A, *B;
+        float *A = x_out, *B = tmpx;
         const char *pi = (const char*)x_init, *po = (const char*)x_out;
         if (pi == po) {  // in-place request: iterate from a copy (Jacobi needs two buffers)
             MM_CU(cudaMemcpyAsync(tmpx, x_init, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
             src = tmpx;
-            A = x_out;
-            B = tmpx;
         } else if (pi < po + xbytes && po < pi + xbytes) {
-            set_err("mm_layout: x_init partially overlaps x_out");
+            set_err("%s: x_init partially overlaps x_out", who);
             return MM_ERR_INVALID_ARGUMENT;
-        } else {
-            A = (K % 2 == 1) ? x_out : tmpx;
-            B = (A == x_out) ? tmpx : x_out;
         }
         const float* res = nullptr;
+        int32_t nsw = 0;
         trace("layout: sweeps enqueue");
-        MM_CU(run_sweeps(S, dim, alpha, q, nullptr, src, A, B, K, dstats, sb, ls, &res), "mm_layout sweeps");
+        if ((s = run.run(S, dim, q, nullptr, src, A, B, dstats, sb, ls, 0, false, &res, &nsw)) != MM_OK) return s;
         trace("layout: sweeps enqueued");
         if (res != x_out) MM_CU(cudaMemcpyAsync(x_out, res, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
         mm_sweep_stats hs;
@@ -998,13 +1049,17 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
         trace("layout: sweeps done (synced)");
         R.levels = 1;
         R.n_level[0] = n0;
+        R.sweeps_level[0] = nsw;
         R.rel_change = hs.x2 > 0 ? sqrt(hs.dx2 / hs.x2) : INFINITY;
-        R.vertex_updates = (int64_t)n0 * K;
-        R.pair_interactions = (int64_t)n0 * (n0 - 1) * K;
-        if (hs.flags & 1) { set_err("mm_layout: non-finite coordinate produced"); return MM_ERR_NONFINITE; }
+        R.vertex_updates = (int64_t)n0 * nsw;
+        R.pair_interactions = (int64_t)n0 * (n0 - 1) * nsw;
+        if (hs.flags & 1) { set_err("%s: non-finite coordinate produced", who); return MM_ERR_NONFINITE; }
     } else {
         mm_hierarchy* H = nullptr;
-        if ((s = build_hierarchy_impl(g, nullptr, dim, seed, n_stop, MM_MAX_LEVELS, 64, &H, ls)) != MM_OK) return s;
+        // dynamic update: "stop the coarsening process after the computation of h levels"
+        const int32_t max_levels = dynamic ? std::min(h + 1, (int)MM_MAX_LEVELS) : MM_MAX_LEVELS;
+        if ((s = build_hierarchy_impl(g, nullptr, dim, seed, dynamic ? 1 : n_stop, max_levels, 64, &H, ls)) != MM_OK)
+            return s;
         struct HGuard {
             mm_hierarchy* h;
             ~HGuard() { mm_hierarchy_free(h); }
@@ -1022,16 +1077,17 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
             t.w = H->lv[l].w;
             return t;
         };
-        // workspace = max over levels
+        const int32_t lo_level = 0, hi_level = dynamic ? 0 : L;  // levels optimized
+        // workspace = max over the optimized levels
         size_t wsb = 0;
-        for (int32_t l = 0; l <= L; ++l) {
+        for (int32_t l = lo_level; l <= hi_level; ++l) {
             const int32_t hp = std::min(h, L - l);
-            const int32_t k = (l == L) ? 0 : H->lv[l + hp].n;
-            wsb = std::max(wsb, sweep_bytes(H->lv[l].n, dim, k, l != L, 1.0));
+            const int32_t k = hp > 0 ? H->lv[l + hp].n : 0;
+            wsb = std::max(wsb, sweep_bytes(H->lv[l].n, dim, k, hp > 0, 1.0));
         }
         const size_t need = wsb + 2 * al(xbytes) + 2 * al((size_t)n0 * 4) + al(sizeof(mm_sweep_stats)) + al(64);
         DevBuf buf(need, ls);
-        if (!buf.p) { set_err("mm_layout: out of device memory (%zu B)", need); return MM_ERR_OUT_OF_MEMORY; }
+        if (!buf.p) { set_err("%s: out of device memory (%zu B)", who, need); return MM_ERR_OUT_OF_MEMORY; }
         Carver cv(buf.p, need);
         float* xa = cv.take<float>((size_t)n0 * st_w);
         float* xb = cv.take<float>((size_t)n0 * st_w);
@@ -1041,65 +1097,74 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
         double* dsum = cv.take<double>(8);
         const size_t ws_off = cv.off;
         MM_CU(cudaMemsetAsync(dstats, 0, sizeof(mm_sweep_stats), ls), "mm_layout memset");
-        // coarsest level: box init + exact sweeps (Q13, Q14)
-        {
+        const float* cur = nullptr;
+        if (dynamic) {
+            MM_CU(cudaMemcpyAsync(xa, x_init, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
+            cur = xa;
+        } else {
+            // coarsest level: box init (Q14), then the level's sweeps (exact, Q13)
             mm_sset SL = S_of(L);
-            const int32_t nL = SL.n;
-            MM_CU(launch_init_box(dim, nL, SL.d, SL.nnz, dsum, seed, L, xa, ls), "mm_layout init");
-            Carver wc((char*)buf.p + ws_off, need - ws_off);
-            SweepBufs sb;
-            if (!carve_sweep(wc, nL, dim, 0, false, 1.0, sb)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
-            MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
-            const float* res = nullptr;
-            MM_CU(run_sweeps(&SL, dim, alpha, q, nullptr, xa, xb, xa, K_of(L), dstats, sb, ls, &res), "mm_layout coarsest");
-            R.n_level[L] = nL;
-            R.k_level[L] = 0;
-            R.vertex_updates += (int64_t)nL * K_of(L);
-            R.pair_interactions += (int64_t)nL * (nL - 1) * K_of(L);
-            const float* cur = res;
-            for (int32_t l = L - 1; l >= 0; --l) {
-                const int32_t nf = H->lv[l].n;
+            MM_CU(launch_init_box(dim, SL.n, SL.d, SL.nnz, dsum, seed, L, xa, ls), "mm_layout init");
+            cur = xa;
+        }
+        for (int32_t l = hi_level; l >= lo_level; --l) {
+            const int32_t nf = H->lv[l].n;
+            if (!dynamic && l < L) {
                 float* dst = (cur == xa) ? xb : xa;
                 MM_CU(launch_prolong(dim, nf, H->lv[l].parent, cur, seed, l, dst, ls), "mm_layout prolong");
                 cur = dst;
-                const int32_t hp = std::min(h, L - l);
+            }
+            const int32_t hp = std::min(h, L - l);
+            mm_approx ap;
+            mm_approx* app = nullptr;
+            if (hp > 0) {
                 // H = parent_{l+hp-1} o ... o parent_l
                 MM_CU(cudaMemcpyAsync(anc, H->lv[l].parent, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, ls), "mm_layout anc");
                 for (int32_t t = 1; t < hp; ++t) {
                     MM_CU(launch_compose(nf, anc, H->lv[l + t].parent, anc2, ls), "mm_layout compose");
                     std::swap(anc, anc2);
                 }
-                mm_approx ap;
                 ap.k = H->lv[l + hp].n;
                 ap.parent = H->lv[l].parent;
                 ap.ancestor = anc;
-                mm_sset Sl = S_of(l);
-                Carver wl((char*)buf.p + ws_off, need - ws_off);
-                SweepBufs sbl;
-                if (!carve_sweep(wl, nf, dim, ap.k, true, 1.0, sbl)) { set_err("mm_layout: carving failed"); return MM_ERR_INVALID_ARGUMENT; }
-                MM_CU(cudaMemsetAsync(sbl.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
-                MM_CU(prepare_approx(nf, &ap, sbl, ls), "mm_layout prepare_approx");
-                float* other = (cur == xa) ? xb : xa;
-                MM_CU(run_sweeps(&Sl, dim, alpha, q, &ap, cur, other, (float*)cur, K_of(l), dstats, sbl, ls, &res),
-                      "mm_layout sweeps");
-                cur = res;
-                R.n_level[l] = nf;
-                R.k_level[l] = ap.k;
-                R.vertex_updates += (int64_t)nf * K_of(l);
-                R.pair_interactions += ((int64_t)nf * (ap.k - 1) + 2 * (int64_t)(nf - H->lv[l + 1].n)) * K_of(l);
+                app = &ap;
             }
-            MM_CU(cudaMemcpyAsync(x_out, cur, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
+            mm_sset Sl = S_of(l);
+            Carver wl((char*)buf.p + ws_off, need - ws_off);
+            SweepBufs sbl;
+            if (!carve_sweep(wl, nf, dim, app ? ap.k : 0, app != nullptr, 1.0, sbl)) {
+                set_err("%s: carving failed", who);
+                return MM_ERR_INVALID_ARGUMENT;
+            }
+            MM_CU(cudaMemsetAsync(sbl.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
+            if (app) MM_CU(prepare_approx(nf, app, sbl, ls), "mm_layout prepare_approx");
+            float* other = (cur == xa) ? xb : xa;
+            const float* res = nullptr;
+            int32_t nsw = 0;
+            if ((s = run.run(&Sl, dim, q, app, cur, other, (float*)cur, dstats, sbl, ls, l, dynamic, &res, &nsw)) !=
+                MM_OK)
+                return s;
+            cur = res;
+            R.n_level[l] = nf;
+            R.k_level[l] = app ? ap.k : 0;
+            R.sweeps_level[l] = nsw;
+            R.vertex_updates += (int64_t)nf * nsw;
+            if (app)
+                R.pair_interactions += ((int64_t)nf * (ap.k - 1) + 2 * (int64_t)(nf - H->lv[l + 1].n)) * nsw;
+            else
+                R.pair_interactions += (int64_t)nf * (nf - 1) * nsw;
         }
+        MM_CU(cudaMemcpyAsync(x_out, cur, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout copy");
         mm_sweep_stats hs;
         MM_CU(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, ls), "mm_layout d2h");
         MM_CU(cudaStreamSynchronize(ls), "mm_layout sync");
         R.rel_change = hs.x2 > 0 ? sqrt(hs.dx2 / hs.x2) : INFINITY;
-        if (hs.flags & 1) { set_err("mm_layout: non-finite coordinate produced"); return MM_ERR_NONFINITE; }
+        if (hs.flags & 1) { set_err("%s: non-finite coordinate produced", who); return MM_ERR_NONFINITE; }
     }
     double en[3] = {0, 0, 0};
     int64_t coinc = 0;
     trace("layout: energy begin");
-    s = energy_core(S, dim, alpha, q, x_out, en, ls, false, &coinc);
+    s = energy_core(S, dim, alpha_energy, q, x_out, en, ls, false, &coinc);
     trace("layout: energy done");
     R.coincident_pairs = coinc;
     R.stress = en[0];
@@ -1110,4 +1175,61 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
     MM_CU(cudaEventRecord(ev, ls), "mm_layout event");
     MM_CU(cudaStreamWaitEvent(us, ev, 0), "mm_layout wait");
     return s;
+}
+
+}  // namespace
+
+extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, float alpha, float q, int h,
+                               const int32_t* sweeps, int32_t nsweeps, uint64_t seed, int32_t n_stop,
+                               const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_sset(S, "mm_layout")) != MM_OK) return s;
+    if ((s = check_dim_q(dim, q, "mm_layout")) != MM_OK) return s;
+    if ((s = check_x(x_out, dim, "x_out", "mm_layout")) != MM_OK) return s;
+    if (!sweeps || nsweeps < 1 || h < 0 || !isfinite(alpha)) {
+        set_err("mm_layout: bad arguments (sweeps host array with nsweeps >= 1, h >= 0, finite alpha)");
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    for (int32_t t = 0; t < nsweeps; ++t)
+        if (sweeps[t] < 0) { set_err("mm_layout: negative sweep count"); return MM_ERR_INVALID_ARGUMENT; }
+    if (h == 0 && (s = check_x(x_init, dim, "x_init", "mm_layout")) != MM_OK) return s;
+    if (h > 0) {
+        if ((s = check_graph(g, "mm_layout")) != MM_OK) return s;
+        if (g->n != S->n) { set_err("mm_layout: graph and S sizes differ"); return MM_ERR_INVALID_ARGUMENT; }
+        if (n_stop < 1) { set_err("mm_layout: n_stop must be >= 1"); return MM_ERR_INVALID_ARGUMENT; }
+    }
+    FixedRunner fr;
+    fr.alpha = alpha;
+    fr.sweeps = sweeps;
+    fr.nsweeps = nsweeps;
+    return layout_impl(g, S, dim, q, h, fr, alpha, seed, n_stop, h > 0 ? MM_LAYOUT_MULTILEVEL : 0, x_init, x_out, rep,
+                       (cudaStream_t)stream, "mm_layout");
+}
+
+extern "C" mm_status mm_layout_schedule(const mm_graph* g, const mm_sset* S, int dim, float q, int h,
+                                        const mm_schedule* sch, uint64_t seed, int32_t n_stop, int32_t flags,
+                                        const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream) {
+    mm_status s;
+    const char* who = "mm_layout_schedule";
+    if ((s = check_sset(S, who)) != MM_OK) return s;
+    if ((s = check_dim_q(dim, q, who)) != MM_OK) return s;
+    if ((s = check_x(x_out, dim, "x_out", who)) != MM_OK) return s;
+    if (!sch || h < 0 || sch->a < 1 || sch->max_final_iters < 1 || !(sch->alpha_min > 0.0) ||
+        !(sch->alpha0 >= sch->alpha_min) || !(sch->factor > 0.0 && sch->factor < 1.0) || !(sch->eps >= 0.0) ||
+        (flags & ~(MM_LAYOUT_MULTILEVEL | MM_LAYOUT_DYNAMIC)) != 0) {
+        set_err("%s: bad arguments (schedule: a >= 1, max_final_iters >= 1, 0 < alpha_min <= alpha0, "
+                "0 < factor < 1, eps >= 0; h >= 0; flags)", who);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    const bool multilevel = (flags & MM_LAYOUT_MULTILEVEL) != 0, dynamic = (flags & MM_LAYOUT_DYNAMIC) != 0;
+    if ((!multilevel || dynamic) && (s = check_x(x_init, dim, "x_init", who)) != MM_OK) return s;
+    if (multilevel || dynamic) {
+        if ((s = check_graph(g, who)) != MM_OK) return s;
+        if (g->n != S->n) { set_err("%s: graph and S sizes differ", who); return MM_ERR_INVALID_ARGUMENT; }
+        if (n_stop < 1) { set_err("%s: n_stop must be >= 1", who); return MM_ERR_INVALID_ARGUMENT; }
+    }
+    ScheduleRunner sr;
+    sr.sch = *sch;
+    return layout_impl(g, S, dim, q, h, sr, sch->alpha_min, seed, n_stop, flags, x_init, x_out, rep,
+                       (cudaStream_t)stream, who);
 }

@@ -23,7 +23,8 @@ MM_MAX_LEVELS = 64
 
 EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator", "mm_sweep_workspace",
            "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_hierarchy_num_levels", "mm_hierarchy_level",
-           "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_launch_count", "mm_profile_enable",
+           "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_launch_count",
+           "mm_profile_enable",
            "mm_profile_reset", "mm_profile_read"]
 
 
@@ -65,7 +66,22 @@ class mm_layout_report(ctypes.Structure):
                 ("k_level", ctypes.c_int32 * MM_MAX_LEVELS), ("stress", ctypes.c_double),
                 ("entropy", ctypes.c_double), ("energy", ctypes.c_double), ("rel_change", ctypes.c_double),
                 ("vertex_updates", ctypes.c_int64), ("pair_interactions", ctypes.c_int64),
-                ("coincident_pairs", ctypes.c_int64)]
+                ("coincident_pairs", ctypes.c_int64), ("sweeps_level", ctypes.c_int32 * MM_MAX_LEVELS)]
+
+
+class mm_schedule(ctypes.Structure):
+    _fields_ = [("alpha0", ctypes.c_double), ("alpha_min", ctypes.c_double), ("factor", ctypes.c_double),
+                ("eps", ctypes.c_double), ("a", ctypes.c_int32), ("max_final_iters", ctypes.c_int32)]
+
+
+MM_LAYOUT_MULTILEVEL, MM_LAYOUT_DYNAMIC = 1, 2
+
+
+def paper_schedule(**kw) -> mm_schedule:
+    """The paper's defaults; max_final_iters is a safety cap."""
+    v = dict(alpha0=1.0, alpha_min=0.008, factor=0.3, eps=1e-4, a=2, max_final_iters=200)
+    v.update(kw)
+    return mm_schedule(**v)
 
 
 class mm_kernel_profile(ctypes.Structure):
@@ -106,6 +122,9 @@ def load() -> ctypes.CDLL:
     L.mm_layout.argtypes = [P(mm_graph), P(mm_sset), ctypes.c_int, f32, f32, ctypes.c_int, P(i32), i32, u64, i32,
                             vp, vp, P(mm_layout_report), vp]
     L.mm_layout.restype = ctypes.c_int
+    L.mm_layout_schedule.argtypes = [P(mm_graph), P(mm_sset), ctypes.c_int, f32, ctypes.c_int, P(mm_schedule), u64, i32,
+                                     i32, vp, vp, P(mm_layout_report), vp]
+    L.mm_layout_schedule.restype = ctypes.c_int
     L.mm_launch_count.argtypes = []; L.mm_launch_count.restype = i64
     L.mm_profile_enable.argtypes = [ctypes.c_int]; L.mm_profile_enable.restype = ctypes.c_int
     L.mm_profile_reset.argtypes = []; L.mm_profile_reset.restype = ctypes.c_int
@@ -317,11 +336,37 @@ def layout(g: Optional[DeviceGraph], S: DeviceSSet, dim: int, alpha: float, q: f
                      int(h), sw, len(sweeps), int(seed), int(n_stop), _ptr(x_init), _ptr(out), ctypes.byref(rep),
                      _stream_ptr(device))
     _check(rc, "mm_layout")
-    r = {"levels": rep.levels, "n_level": list(rep.n_level[:rep.levels]),
-         "k_level": list(rep.k_level[:rep.levels]), "stress": rep.stress, "entropy": rep.entropy,
-         "energy": rep.energy, "rel_change": rep.rel_change, "vertex_updates": rep.vertex_updates,
-         "pair_interactions": rep.pair_interactions, "coincident_pairs": rep.coincident_pairs}
-    return out, r
+    return out, _report(rep)
+
+
+def _report(rep: mm_layout_report) -> dict:
+    return {"levels": rep.levels, "n_level": list(rep.n_level[:rep.levels]),
+            "k_level": list(rep.k_level[:rep.levels]), "sweeps_level": list(rep.sweeps_level[:rep.levels]),
+            "stress": rep.stress, "entropy": rep.entropy, "energy": rep.energy, "rel_change": rep.rel_change,
+            "vertex_updates": rep.vertex_updates, "pair_interactions": rep.pair_interactions,
+            "coincident_pairs": rep.coincident_pairs}
+
+
+def layout_schedule(g: Optional[DeviceGraph], S: DeviceSSet, dim: int, q: float, h: int, sched: mm_schedule,
+                    seed: int, n_stop: int = 1000, multilevel: bool = True, dynamic: bool = False, x_init=None,
+                    out=None):
+    """The paper's alpha schedule or the dynamic update.
+    Returns (x_out tensor, report dict incl. sweeps_level)."""
+    torch = _torch()
+    L = load()
+    n = S.n
+    device = S.row_ptr.device
+    if out is None:
+        out = torch.empty((n, 2 if dim == 2 else 4), dtype=torch.float32, device=device)
+    rep = mm_layout_report()
+    gs = g.c_struct() if g is not None else None
+    s = S.c_struct()
+    flags = (MM_LAYOUT_MULTILEVEL if multilevel else 0) | (MM_LAYOUT_DYNAMIC if dynamic else 0)
+    rc = L.mm_layout_schedule(ctypes.byref(gs) if gs is not None else None, ctypes.byref(s), dim, float(q), int(h),
+                              ctypes.byref(sched), int(seed), int(n_stop), flags, _ptr(x_init), _ptr(out),
+                              ctypes.byref(rep), _stream_ptr(device))
+    _check(rc, "mm_layout_schedule")
+    return out, _report(rep)
 
 
 def launch_count() -> int:

@@ -1,0 +1,96 @@
+"""Pins for the oracle's schedule driver and dynamic
+update: the round structure is checked against a hand-written
+decision trace of the paper's rules on top of the (pinned) oracle sweep."""
+from __future__ import annotations
+
+import numpy as np
+
+import oracle
+from tests import helpers as H
+from workloads import configs, dynamic, graphs
+
+
+def test_alpha_sequence_clamped():
+    """1, 0.3, 0.09, 0.027, 0.0081, then 0.008 (reading R2)."""
+    a, seq = 1.0, []
+    while True:
+        seq.append(a)
+        if a <= 0.008:
+            break
+        a = max(a * 0.3, 0.008)
+    np.testing.assert_allclose(seq, [1, 0.3, 0.09, 0.027, 0.0081, 0.008], rtol=1e-12)
+
+
+def _schedule_by_hand(S, x, q, sch):
+    """The paper's rules re-stated literally around oracle.sweep_exact."""
+    alpha, trace = sch.alpha0, []
+    while True:
+        final = alpha <= sch.alpha_min
+        for _ in range(sch.max_final_iters if final else sch.a):
+            y = oracle.sweep_exact(S, x, alpha, q)
+            rel = np.linalg.norm(y - x) / np.linalg.norm(x)
+            trace.append(alpha)
+            x = y
+            if rel < sch.eps:
+                break
+        if final:
+            return x, trace
+        alpha = max(alpha * sch.factor, sch.alpha_min)
+
+
+def test_single_level_schedule_matches_literal_rules():
+    w = configs.make("cfg2_rgg1024")
+    sch = oracle.paper_schedule(max_final_iters=30)
+    x0 = w.x0.astype(np.float64)
+    x, e, nl, sw = oracle.layout_schedule(w.graph, w.S, 2, 0.0, 0, sch, w.seed, multilevel=False, x_init=x0)
+    xr, trace = _schedule_by_hand(w.S, x0, 0.0, sch)
+    assert nl == 1 and sw[0] == len(trace)
+    np.testing.assert_array_equal(x, xr)
+    np.testing.assert_allclose(e, oracle.energy(w.S, xr, 0.008, 0.0), rtol=0)
+
+
+def test_converged_path_stops_after_one_sweep_per_round():
+    """A fixed point of every alpha is impossible, but a K2 at distance d with no
+    non-S pairs is a fixed point for all alpha: each round stops after 1 sweep."""
+    g = H.path(2)
+    S = H.sset_with(g, np.ones(2))
+    x0 = np.array([[0.0, 0.0], [1.0, 0.0]])
+    x, e, nl, sw = oracle.layout_schedule(g, S, 2, 0.0, 0, oracle.paper_schedule(), 1, multilevel=False, x_init=x0)
+    assert sw[0] == 6  # six rounds (R2), one sweep each
+    np.testing.assert_array_equal(x, x0)
+
+
+def test_multilevel_schedule_levels_and_sweeps():
+    w = configs.make("cfg3_mesh32")
+    sch = oracle.paper_schedule(max_final_iters=20)
+    x, e, nl, sw = oracle.layout_schedule(w.graph, w.S, 2, 0.0, 2, sch, w.seed, n_stop=100)
+    assert nl >= 3 and np.all(sw >= 6) and np.all(sw <= 5 * 2 + 20)
+    assert np.all(np.isfinite(x))
+
+
+def test_dynamic_update_runs_finest_level_only():
+    w = configs.make("cfg3_mesh32")
+    sch = oracle.paper_schedule(max_final_iters=15)
+    x, _, _, _ = oracle.layout_schedule(w.graph, w.S, 2, 0.0, 2, sch, w.seed, n_stop=100)
+    gq = dynamic.perturb(w.graph, 5.0, 2, seed=3)
+    from workloads import sset
+    Sq = sset.hop2_sset(gq)
+    y, e, nl, sw = oracle.layout_schedule(gq, Sq, 2, 0.0, 2, sch, w.seed, dynamic=True, x_init=x)
+    assert nl == 3 and sw[0] >= 1 and np.all(sw[1:] == 0) and sw[0] <= sch.max_final_iters
+    # alpha_min from the start: the first sweep equals a plain Eq.(3) sweep at 0.008
+    lv = oracle.build_hierarchy(gq, seed=w.seed, n_stop=1, max_levels=3)
+    anc = oracle.ancestor(lv, 0, 2)
+    y1 = oracle.sweep_approx(Sq, x, 0.008, 0.0, lv[0].parent, anc, lv[2].n)
+    y1b, _, _, sw1 = oracle.layout_schedule(gq, Sq, 2, 0.0, 2, oracle.paper_schedule(max_final_iters=1), w.seed,
+                                            dynamic=True, x_init=x)
+    assert sw1[0] == 1
+    np.testing.assert_array_equal(y1, y1b)
+
+
+def test_perturbation_model():
+    g = graphs.grid2d(20, 20)
+    q = dynamic.perturb(g, 5.0, 2, seed=1)
+    assert q.n == g.n
+    from scipy.sparse.csgraph import connected_components
+    assert connected_components(q.to_scipy(), directed=False)[0] == 1
+    assert abs(q.m - g.m) <= 2
