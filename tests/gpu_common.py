@@ -45,3 +45,20 @@ def sample_rows(n: int, count: int, seed: int, extra=()) -> np.ndarray:
     rows = rng.choice(n, size=min(count, n), replace=False)
     rows = np.unique(np.concatenate([rows, np.asarray(extra, dtype=np.int64), [0, n - 1]]))
     return rows.astype(np.int32)
+
+
+def rel_diff(a: float, b: float) -> float:
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def assert_energy_or_chaos(e_gpu: float, e_oracle: float, control, what: str, factor: float = 4.0):
+    """Full-run parity (Q20): |E_gpu - E_oracle| <= 1e-3 |E_oracle|, or, if the
+    trajectory is chaotic, within `factor` x the divergence of the oracle from
+    itself under a 1e-7 relative perturbation (control(s) -> oracle energy
+    with the perturbation s)."""
+    rel = rel_diff(e_gpu, e_oracle)
+    if rel <= ENERGY_TOL:
+        return
+    ctrl = max(rel_diff(control(s), e_oracle) for s in (1e-7, -1e-7))
+    assert rel <= factor * ctrl, (what, rel, ctrl)
+    print(f"{what}: |E_gpu - E_oracle| / |E| = {rel:.2e} > {ENERGY_TOL}; chaos control {ctrl:.2e}")
