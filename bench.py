@@ -201,6 +201,13 @@ def run_reference(args):
 
 
 def config_block(w, args):
+    if getattr(args, "schedule", False):
+        desc = (f"{w.name}: the paper's full optimizer MulMent_{args.h} (multilevel, alpha 1 -> x0.3 -> 0.008, "
+                f"a=2, eps=1e-4, cap {args.max_final_iters} sweeps at alpha_min; n={w.n}, |S|={w.S.nnz}, q={w.q}, "
+                f"dim={w.dim})")
+        return {"workload": desc, "n": w.n, "nnz_S": w.S.nnz, "dim": w.dim, "q": w.q, "h": args.h,
+                "schedule": "paper", "l2": "flushed (256 MB write) between timed steps; per-step CUDA events",
+                "parallelism": f"replicas x{args.gpus}"}
     if w.h == 0:
         desc = (f"{w.name}: BASELINE.json configs[{int(w.name[3]) - 1 if w.name[3].isdigit() else '?'}] "
                 f"(n={w.n}, |S|={w.S.nnz}, q={w.q}, alpha={w.alpha}, dim={w.dim}, {w.sweeps} exact sweeps + energy)")
@@ -238,8 +245,16 @@ def run_gpu(args):
         x0 = mm.coords_to_device(w.x0, dev) if w.h == 0 else None
         out = torch.empty((n, 2 if w.dim == 2 else 4), dtype=torch.float32, device=dev)
 
-        def step():
-            return mm.layout(G, S, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=x0, out=out)
+        if args.schedule:
+            # the paper's full optimizer (MulMent_h): multilevel, alpha schedule, h from --h
+            G = mm.graph_to_device(w.graph, dev)
+            sched = mm.paper_schedule(max_final_iters=args.max_final_iters)
+
+            def step():
+                return mm.layout_schedule(G, S, w.dim, w.q, args.h, sched, w.seed, out=out)
+        else:
+            def step():
+                return mm.layout(G, S, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=x0, out=out)
 
         for _ in range(args.warmup):
             _, rep = step()
@@ -287,7 +302,10 @@ def run_gpu(args):
         def e2e_step():
             for hd, dd in zip(hosts, devs):
                 dd.copy_(hd, non_blocking=True)
-            y, r = mm.layout(Ge, Se, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=xe, out=out)
+            if args.schedule:
+                y, r = mm.layout_schedule(G, Se, w.dim, w.q, args.h, sched, w.seed, out=out)
+            else:
+                y, r = mm.layout(Ge, Se, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=xe, out=out)
             h_out.copy_(y, non_blocking=True)
             return r
 
@@ -306,17 +324,20 @@ def run_gpu(args):
     units = sum_over_ranks(float(rep["vertex_updates"]), dev)
     value = units / (ms_step / 1e3)
     pairs_step = rep["pair_interactions"]
-    kname = "repulse_exact" if w.h == 0 else "repulse_coarse"
+    hh = args.h if args.schedule else w.h
+    kname = "repulse_exact" if hh == 0 else "repulse_coarse"
     kern = prof.get(kname, {"launches": 0, "total_ms": float("nan")})
     k_ms = kern["total_ms"] / max(kern["launches"], 1)
     # algorithmic pairs per launch: exact n(n-1) per sweep; coarse: the
     # per-step pair count minus the exact coarsest level, averaged per launch
-    if w.h == 0:
+    if hh == 0 and not args.schedule:
         pairs_launch = n * (n - 1)
+    elif hh == 0:
+        pairs_launch = pairs_step / max(kern["launches"] / args.steps, 1)
     else:
         nL = rep["n_level"][-1]
         pairs_launch = (pairs_step - nL * (nL - 1) * K) / max(kern["launches"] / args.steps, 1)
-    flop_pair = FLOP_PER_PAIR if w.h == 0 else FLOP_PER_PAIR_COARSE
+    flop_pair = FLOP_PER_PAIR if hh == 0 else FLOP_PER_PAIR_COARSE
     if w.q != 0.0:
         flop_pair += 3
     achieved_tflops = flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
@@ -334,7 +355,7 @@ def run_gpu(args):
     if rank != 0:
         return 0
     cpu = None
-    if ws == 1 and not args.no_cpu_baseline and w.h == 0:
+    if ws == 1 and not args.no_cpu_baseline and w.h == 0 and not args.schedule:
         import oracle
 
         rows, cores = cpu_oracle_sample(w, target_s=args.cpu_s)
@@ -383,6 +404,10 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=10.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--schedule", action="store_true",
+                    help="time the paper's full optimizer (alpha schedule, multilevel MulMent_h) instead")
+    ap.add_argument("--h", type=int, default=0, help="approximation depth for --schedule (0 = MulMent_0)")
+    ap.add_argument("--max-final-iters", type=int, default=200)
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "mm":
         print("warning: the contract asks for >= 3 warm-up steps", file=sys.stderr)
