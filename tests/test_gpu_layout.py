@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from tests import helpers as H
-from tests.gpu_common import ENERGY_TOL, workload
+from tests.gpu_common import ENERGY_TOL, assert_energy_or_chaos, workload
 from workloads import configs
 
 pytestmark = pytest.mark.gpu
@@ -97,17 +97,12 @@ def test_layout_multilevel_full_run(mm, name, n_stop):
     assert rep["levels"] == nl
     eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), w.alpha, w.q)
     assert _rel(rep["energy"], eg[2]) <= 1e-4, (rep["energy"], eg)
-    rel = _rel(rep["energy"], eo[2])
-    if rel > ENERGY_TOL:
-        # Q20 chaos control: the oracle against itself with alpha perturbed by
-        # +-1e-7 relative.  A trajectory that diverges this much on its own is
-        # chaotic; the GPU (FP32 rounding ~1e-7 per op) must then stay within a
-        # small factor of that divergence, and its layout's energy must agree
-        # with the oracle's evaluation of it (checked above).
-        ctrl = max(_rel(oracle.layout(w.graph, w.S, w.dim, w.alpha * (1 + s), w.q, w.h, [w.sweeps], w.seed,
-                                      n_stop=n_stop)[1][2], eo[2]) for s in (1e-7, -1e-7))
-        assert rel <= 4.0 * ctrl, (name, rel, ctrl)
-        print(f"{name}: |E_gpu - E_oracle| / |E| = {rel:.2e} > {ENERGY_TOL}; chaos control {ctrl:.2e}")
+
+    def control(s):
+        return oracle.layout(w.graph, w.S, w.dim, w.alpha * (1 + s), w.q, w.h, [w.sweeps], w.seed,
+                             n_stop=n_stop)[1][2]
+
+    assert_energy_or_chaos(rep["energy"], eo[2], control, name)
 
 
 def test_layout_in_place(mm):
