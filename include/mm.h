@@ -233,6 +233,16 @@ MM_API mm_status mm_layout_schedule(const mm_graph* g, const mm_sset* S, int dim
                                     const mm_schedule* sch, uint64_t seed, int32_t n_stop, int32_t flags,
                                     const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream);
 
+/* Full stress, the paper's quality metric:
+ * F(x) = sum over unordered pairs u<v of w_uv (|x_u - x_v| - d_uv)^2 with d_uv
+ * the shortest-path (hop) distance in g and w = d^-2, and the optimal scale
+ * s* = argmin_s F(s x) = A/B (A = sum w d l, B = sum w l^2; reading R5).
+ * out: HOST double[4] = {F(x), s*, F(s* x), number of pairs}.  One BFS per
+ * source (n BFS traversals, O(n m) work); n <= 1,638,400 (visited bitset in
+ * shared memory).  FP64 sums; their order follows the BFS claim order, so the
+ * last bits may vary between runs.  syncs. */
+MM_API mm_status mm_full_stress(const mm_graph* g, int dim, const float* x, double* out, mm_stream_t stream);
+
 /* ------------------------------------------------------------------ instrumentation */
 /* Total kernels launched by this library since load (host counter). */
 MM_API int64_t mm_launch_count(void);

@@ -30,7 +30,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["rng.c", "sweep.c", "energy.c", "hierarchy.c", "layout.c", "schedule.c"]
+_SRCS = ["rng.c", "sweep.c", "energy.c", "hierarchy.c", "layout.c", "schedule.c", "fullstress.c"]
 
 OR_EINVAL, OR_ERHO, OR_ECOINC, OR_ENOMEM = -1, -2, -3, -4
 TAG_INIT, TAG_JITTER, TAG_MATCH = 0x494E4954, 0x4A495454, 0x4D415443
@@ -105,6 +105,7 @@ def lib() -> ctypes.CDLL:
     L.or_layout_schedule.argtypes = [c_i32, c_int, _i64p, _i32p, _i64p, _i32p, _f64p, _f64p, c_dbl, c_int,
                                      ctypes.POINTER(Schedule), c_u64, c_i32, c_int, _f64p, _f64p, _f64p, _i32p, _i32p,
                                      c_int]
+    L.or_full_stress.argtypes = [c_i32, _i64p, _i32p, c_int, _f64p, _f64p, c_int]
     _lib = L
     return L
 
@@ -346,3 +347,16 @@ def layout_schedule(g, S, dim: int, q: float, h: int, sched: Schedule, seed: int
                                     _p(out, ctypes.c_double), _p(en, ctypes.c_double), ctypes.byref(nl),
                                     _p(sw, ctypes.c_int32), nthreads or default_threads()), "layout_schedule")
     return out, (float(en[0]), float(en[1]), float(en[2])), nl.value, sw[:nl.value].copy()
+
+
+def full_stress(g, x: np.ndarray, nthreads: Optional[int] = None):
+    """F(x), the optimal scale s* and F(s* x) over unordered pairs.
+    Returns (F, s_opt, F_opt, pairs)."""
+    rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(g.col, dtype=np.int32)
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    n, dim = x.shape
+    out = np.zeros(4, dtype=np.float64)
+    _check(lib().or_full_stress(n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), dim, _p(x, ctypes.c_double),
+                                _p(out, ctypes.c_double), nthreads or default_threads()), "full_stress")
+    return float(out[0]), float(out[1]), float(out[2]), int(out[3])

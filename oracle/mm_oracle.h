@@ -121,6 +121,11 @@ int or_layout_schedule(int32_t n, int dim, const int64_t* rp, const int32_t* col
                        const double* x_init, double* out, double energy_out[3], int32_t* levels_out,
                        int32_t* sweeps_out, int nthreads);
 
+/* ---- full stress F(x) with graph distances and w = d^-2, and the optimal
+ * scale s* = argmin_s F(s x) (reading R5): out = {F(1), s*, F(s*), pairs} */
+int or_full_stress(int32_t n, const int64_t* rp, const int32_t* col, int dim, const double* x, double out[4],
+                   int nthreads);
+
 #define OR_TAG_INIT 0x494e4954ULL   /* "INIT" */
 #define OR_TAG_JITTER 0x4a495454ULL /* "JITT" */
 #define OR_TAG_MATCH 0x4d415443ULL  /* "MATC" */

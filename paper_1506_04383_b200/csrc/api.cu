@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "k_fullstress.cuh"
 #include "k_hier.cuh"
 #include "k_repulse.cuh"
 
@@ -1232,4 +1233,44 @@ extern "C" mm_status mm_layout_schedule(const mm_graph* g, const mm_sset* S, int
     sr.sch = *sch;
     return layout_impl(g, S, dim, q, h, sr, sch->alpha_min, seed, n_stop, flags, x_init, x_out, rep,
                        (cudaStream_t)stream, who);
+}
+
+// ================================================================== full stress (f4)
+extern "C" mm_status mm_full_stress(const mm_graph* g, int dim, const float* x, double* out, mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_graph(g, "mm_full_stress")) != MM_OK) return s;
+    if (dim != 2 && dim != 3) { set_err("mm_full_stress: dim must be 2 or 3"); return MM_ERR_UNSUPPORTED; }
+    if ((s = check_x(x, dim, "x", "mm_full_stress")) != MM_OK) return s;
+    if (!out) { set_err("mm_full_stress: out is NULL"); return MM_ERR_INVALID_ARGUMENT; }
+    const int32_t n = g->n;
+    if (full_stress_smem(n) > 200 * 1024) {
+        set_err("mm_full_stress: n = %d exceeds the shared-memory visited set (n <= 1,638,400)", n);
+        return MM_ERR_UNSUPPORTED;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int grid = full_stress_grid(n);
+    const size_t bytes = al((size_t)grid * 2 * n * sizeof(int32_t)) + al((size_t)grid * 5 * sizeof(double));
+    DevBuf buf(bytes, st);
+    if (!buf.p) { set_err("mm_full_stress: out of device memory (%zu B)", bytes); return MM_ERR_OUT_OF_MEMORY; }
+    Carver cv(buf.p, bytes);
+    int32_t* qbuf = cv.take<int32_t>((size_t)grid * 2 * n);
+    double* partial = cv.take<double>((size_t)grid * 5);
+    MM_CU(launch_full_stress(dim, n, g->row_ptr, g->col, x, grid, qbuf, partial, st), "mm_full_stress");
+    std::vector<double> h((size_t)grid * 5);
+    MM_CU(cudaMemcpyAsync(h.data(), partial, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st), "mm_full_stress d2h");
+    MM_CU(cudaStreamSynchronize(st), "mm_full_stress sync");
+    double A = 0, B = 0, C = 0, F = 0, P = 0;
+    for (int b = 0; b < grid; ++b) {
+        A += h[(size_t)b * 5];
+        B += h[(size_t)b * 5 + 1];
+        C += h[(size_t)b * 5 + 2];
+        F += h[(size_t)b * 5 + 3];
+        P += h[(size_t)b * 5 + 4];
+    }
+    const double sc = B > 0.0 ? A / B : 1.0;
+    out[0] = F;
+    out[1] = sc;
+    out[2] = sc * sc * B - 2.0 * sc * A + C;
+    out[3] = P;
+    return MM_OK;
 }

@@ -23,7 +23,8 @@ MM_MAX_LEVELS = 64
 
 EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator", "mm_sweep_workspace",
            "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_hierarchy_num_levels", "mm_hierarchy_level",
-           "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_launch_count",
+           "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_full_stress",
+           "mm_launch_count",
            "mm_profile_enable",
            "mm_profile_reset", "mm_profile_read"]
 
@@ -125,6 +126,8 @@ def load() -> ctypes.CDLL:
     L.mm_layout_schedule.argtypes = [P(mm_graph), P(mm_sset), ctypes.c_int, f32, ctypes.c_int, P(mm_schedule), u64, i32,
                                      i32, vp, vp, P(mm_layout_report), vp]
     L.mm_layout_schedule.restype = ctypes.c_int
+    L.mm_full_stress.argtypes = [P(mm_graph), ctypes.c_int, vp, P(f64), vp]
+    L.mm_full_stress.restype = ctypes.c_int
     L.mm_launch_count.argtypes = []; L.mm_launch_count.restype = i64
     L.mm_profile_enable.argtypes = [ctypes.c_int]; L.mm_profile_enable.restype = ctypes.c_int
     L.mm_profile_reset.argtypes = []; L.mm_profile_reset.restype = ctypes.c_int
@@ -389,3 +392,12 @@ def profile_read() -> dict:
     L.mm_profile_read(arr, cnt.value, ctypes.byref(cnt))
     return {arr[i].name.decode(): {"launches": int(arr[i].launches), "total_ms": float(arr[i].total_ms)}
             for i in range(cnt.value)}
+
+
+def full_stress(g: DeviceGraph, x):
+    """Full stress F(x), optimal scale s*, F(s* x), pair count."""
+    L = load()
+    out = (ctypes.c_double * 4)()
+    gs = g.c_struct()
+    _check(L.mm_full_stress(ctypes.byref(gs), _dim_of(x), _ptr(x), out, _stream_ptr(x.device)), "mm_full_stress")
+    return float(out[0]), float(out[1]), float(out[2]), int(out[3])

@@ -94,3 +94,47 @@ def test_perturbation_model():
     from scipy.sparse.csgraph import connected_components
     assert connected_components(q.to_scipy(), directed=False)[0] == 1
     assert abs(q.m - g.m) <= 2
+
+
+# ---------------------------------------------------------------- full stress (f4)
+def test_full_stress_worked_examples():
+    """SPEC S:325-326 examples re-derived: path-3 at 0,1,2 -> F = 0 (the pair
+    (0,2) has length 2 = d); K2 at distance 3 -> F = (3-1)^2 = 4."""
+    g = H.path(3)
+    F, s, Fs, P = oracle.full_stress(g, np.array([[0.0, 0], [1, 0], [2, 0]]))
+    assert F == 0.0 and P == 3 and s == 1.0
+    F, s, Fs, P = oracle.full_stress(H.path(2), np.array([[0.0, 0], [3, 0]]))
+    assert F == 4.0 and abs(s - 1 / 3) < 1e-15 and Fs == 0.0
+
+
+def test_full_stress_against_scipy_and_numeric_min():
+    """Distances from scipy's shortest_path (library routine); F(s) minimised
+    numerically (bounded scalar search) agrees with the closed form."""
+    from scipy.optimize import minimize_scalar
+    from scipy.sparse.csgraph import shortest_path
+
+    g = H.random_connected(60, 40, seed=9)
+    x = np.random.default_rng(10).normal(size=(g.n, 2)) * 3
+    D = shortest_path(g.to_scipy(), unweighted=True, directed=False)
+    iu = np.triu_indices(g.n, 1)
+    d = D[iu]
+    l = np.linalg.norm(x[iu[0]] - x[iu[1]], axis=1)
+    F_ref = np.sum((l - d) ** 2 / d ** 2)
+    F, s, Fs, P = oracle.full_stress(g, x)
+    np.testing.assert_allclose(F, F_ref, rtol=1e-12)
+    assert P == iu[0].shape[0]
+    res = minimize_scalar(lambda t: np.sum((t * l - d) ** 2 / d ** 2), bounds=(1e-3, 1e3), method="bounded",
+                          options={"xatol": 1e-12})
+    np.testing.assert_allclose(s, res.x, rtol=1e-6)
+    np.testing.assert_allclose(Fs, res.fun, rtol=1e-9)
+
+
+def test_full_stress_scale_and_rigid_invariance():
+    g = H.random_connected(40, 30, seed=11)
+    x = np.random.default_rng(12).normal(size=(g.n, 3))
+    F, s, Fs, _ = oracle.full_stress(g, x)
+    c, sn = np.cos(0.7), np.sin(0.7)
+    Q = np.array([[c, -sn, 0], [sn, c, 0], [0, 0, 1.0]])
+    F2, s2, Fs2, _ = oracle.full_stress(g, 2.5 * x @ Q.T + 1.0)
+    np.testing.assert_allclose(Fs2, Fs, rtol=1e-10)
+    np.testing.assert_allclose(s2, s / 2.5, rtol=1e-10)
