@@ -138,6 +138,8 @@ typedef struct {
 } mm_schedule;
 #define MM_LAYOUT_MULTILEVEL 1 /* hierarchy + prolongation; h = 0: exact Eq.(2) on every level */
 #define MM_LAYOUT_DYNAMIC 2    /* dynamic update: finest level only, from x_init, at alpha_min */
+#define MM_LAYOUT_SCLAP 4      /* SCLaP hierarchy (reading R6; l = 3, f = 20, b = 2) instead of matching */
+#define MM_LAYOUT_DISC_PROLONG 8 /* the paper's disc prolongation (R7) instead of Q15's jitter */
 
 /* ------------------------------------------------------------------ API */
 
@@ -191,6 +193,16 @@ MM_API mm_status mm_energy(const mm_sset* S, int dim, double alpha, double q, co
 MM_API mm_status mm_build_hierarchy(const mm_graph* g, const int32_t* c, int dim, uint64_t seed,
                              int32_t n_stop, int32_t max_levels, int32_t max_rounds,
                              mm_hierarchy** out, mm_stream_t stream);
+/* The paper's SCLaP hierarchy in the synchronous reading R6 of
+ * level h = 1, 2, ... clusters with size bound U = max(max c,
+ * min(b^h, n/f)) in lp_rounds label-propagation rounds (f0 = 20, b = 2 in the
+ * paper; f <- 0.7 f after a contraction that is not 10% smaller), then
+ * contracts (coarse id = rank of the distinct labels).  Integer-exact: bit-
+ * identical to the oracle.  Stops at n_stop, max_levels or 10 ineffective
+ * decays.  Syncs a few times per round. */
+MM_API mm_status mm_build_hierarchy_sclap(const mm_graph* g, const int32_t* c, int dim, uint64_t seed,
+                                          int32_t n_stop, int32_t max_levels, int32_t lp_rounds, double f0, double b,
+                                          mm_hierarchy** out, mm_stream_t stream);
 MM_API int32_t mm_hierarchy_num_levels(const mm_hierarchy* h);
 MM_API mm_status mm_hierarchy_level(const mm_hierarchy* h, int32_t level, mm_level_view* out /*host*/);
 MM_API void mm_hierarchy_free(mm_hierarchy* h);

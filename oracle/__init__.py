@@ -30,7 +30,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
-_SRCS = ["rng.c", "sweep.c", "energy.c", "hierarchy.c", "layout.c", "schedule.c", "fullstress.c"]
+_SRCS = ["rng.c", "sweep.c", "energy.c", "hierarchy.c", "layout.c", "schedule.c", "fullstress.c", "sclap.c"]
 
 OR_EINVAL, OR_ERHO, OR_ECOINC, OR_ENOMEM = -1, -2, -3, -4
 TAG_INIT, TAG_JITTER, TAG_MATCH = 0x494E4954, 0x4A495454, 0x4D415443
@@ -106,6 +106,9 @@ def lib() -> ctypes.CDLL:
                                      ctypes.POINTER(Schedule), c_u64, c_i32, c_int, _f64p, _f64p, _f64p, _i32p, _i32p,
                                      c_int]
     L.or_full_stress.argtypes = [c_i32, _i64p, _i32p, c_int, _f64p, _f64p, c_int]
+    L.or_build_hierarchy_sclap.argtypes = [c_i32, _i64p, _i32p, _i64p, _i64p, c_u64, c_i32, c_i32, c_i32, c_dbl, c_dbl,
+                                           ctypes.POINTER(ctypes.c_void_p)]
+    L.or_sclap_labels.argtypes = [c_i32, _i64p, _i32p, _i64p, _i64p, c_i64, c_i32, c_u64, c_i32, _i32p]
     _lib = L
     return L
 
@@ -225,17 +228,24 @@ class Level:
 
 
 def build_hierarchy(g, seed: int, n_stop: int = 1000, max_levels: int = 64, max_rounds: int = 64,
-                    omega: Optional[np.ndarray] = None, c: Optional[np.ndarray] = None) -> List[Level]:
-    """Matching-based hierarchy (Q16/Q17), contraction per P:225-232."""
+                    omega: Optional[np.ndarray] = None, c: Optional[np.ndarray] = None, sclap: bool = False,
+                    lp_rounds: int = 3, f0: float = 20.0, b: float = 2.0) -> List[Level]:
+    """Matching-based hierarchy (Q16/Q17) or SCLaP (sclap=True, P:202-223, R6);
+    contraction per P:225-232."""
     rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
     col = np.ascontiguousarray(g.col, dtype=np.int32)
     om = None if omega is None else np.ascontiguousarray(omega, dtype=np.int64)
     cc = None if c is None else np.ascontiguousarray(c, dtype=np.int64)
     h = ctypes.c_void_p()
     L = lib()
-    _check(L.or_build_hierarchy(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
-                                _p(om, ctypes.c_int64), _p(cc, ctypes.c_int64), seed, n_stop,
-                                max_levels, max_rounds, ctypes.byref(h)), "build_hierarchy")
+    if sclap:
+        _check(L.or_build_hierarchy_sclap(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+                                          _p(om, ctypes.c_int64), _p(cc, ctypes.c_int64), seed, n_stop, max_levels,
+                                          lp_rounds, f0, b, ctypes.byref(h)), "build_hierarchy_sclap")
+    else:
+        _check(L.or_build_hierarchy(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+                                    _p(om, ctypes.c_int64), _p(cc, ctypes.c_int64), seed, n_stop,
+                                    max_levels, max_rounds, ctypes.byref(h)), "build_hierarchy")
     try:
         levels = []
         for l in range(L.or_hier_num_levels(h)):
@@ -328,7 +338,7 @@ def layout(g, S, dim: int, alpha: float, q: float, h: int, sweeps, seed: int, n_
 
 def layout_schedule(g, S, dim: int, q: float, h: int, sched: Schedule, seed: int, n_stop: int = 1000,
                     multilevel: bool = True, dynamic: bool = False, x_init: Optional[np.ndarray] = None,
-                    nthreads: Optional[int] = None):
+                    nthreads: Optional[int] = None, sclap: bool = False, disc: bool = False):
     """The paper's schedule or the dynamic update.
     Returns (x0, (stress, entropy, total at alpha_min), levels, sweeps per level)."""
     rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
@@ -340,7 +350,7 @@ def layout_schedule(g, S, dim: int, q: float, h: int, sched: Schedule, seed: int
     en = np.zeros(3, dtype=np.float64)
     nl = ctypes.c_int32()
     sw = np.zeros(64, dtype=np.int32)
-    flags = (1 if multilevel else 0) | (2 if dynamic else 0)
+    flags = (1 if multilevel else 0) | (2 if dynamic else 0) | (4 if sclap else 0) | (8 if disc else 0)
     _check(lib().or_layout_schedule(n, dim, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(srp, ctypes.c_int64),
                                     _p(scol, ctypes.c_int32), _p(d, ctypes.c_double), _p(w, ctypes.c_double), q, h,
                                     ctypes.byref(sched), seed, n_stop, flags, _p(xi, ctypes.c_double),
@@ -360,3 +370,16 @@ def full_stress(g, x: np.ndarray, nthreads: Optional[int] = None):
     _check(lib().or_full_stress(n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), dim, _p(x, ctypes.c_double),
                                 _p(out, ctypes.c_double), nthreads or default_threads()), "full_stress")
     return float(out[0]), float(out[1]), float(out[2]), int(out[3])
+
+
+def sclap_labels(g, U: int, rounds: int, seed: int, level: int, omega=None, c=None) -> np.ndarray:
+    """One SCLaP clustering (R6) with size bound U; returns the labels."""
+    rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
+    col = np.ascontiguousarray(g.col, dtype=np.int32)
+    om = np.ascontiguousarray(np.ones(col.shape[0]) if omega is None else omega, dtype=np.int64)
+    cc = np.ascontiguousarray(np.ones(g.n) if c is None else c, dtype=np.int64)
+    lab = np.empty(g.n, dtype=np.int32)
+    _check(lib().or_sclap_labels(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(om, ctypes.c_int64),
+                                 _p(cc, ctypes.c_int64), U, rounds, seed, level, _p(lab, ctypes.c_int32)),
+           "sclap_labels")
+    return lab

@@ -8,8 +8,8 @@
  * weight of edges that run between block u' and block v'."  Repeated
  * recursively.
  *
- * The clustering itself is BASELINE.json's "seeded heavy-edge matching"
- * (the paper's SCLaP, is out of this build's scope), read as Q16:
+ * The default clustering is BASELINE.json's "seeded heavy-edge matching"
+ * (the paper's SCLaP, is sclap.c + or_build_hierarchy_sclap), read as Q16:
  * a synchronous handshake.  In round r every unmatched u picks the unmatched
  * neighbour v maximising the rating omega_uv / (c_u c_v) — compared exactly
  * as omega_a * c_b  vs  omega_b * c_a in 64-bit integers — ties broken by the
@@ -96,26 +96,35 @@ static int32_t match_level(const or_level* g, uint64_t seed, int32_t level, int3
 }
 
 typedef struct { int32_t col; int64_t w; } centry;
+static int contract_labels(or_level* g, const int32_t* lead, or_level* out);
+
+/* matching: leader = min(u, mate(u)) */
+static int contract_level(or_level* g, const int32_t* mate, or_level* out) {
+    int32_t* lead = (int32_t*)malloc(sizeof(int32_t) * (size_t)(g->n > 0 ? g->n : 1));
+    if (!lead) return OR_ENOMEM;
+    for (int32_t u = 0; u < g->n; ++u) lead[u] = (mate[u] >= 0 && mate[u] < u) ? mate[u] : u;
+    const int rc = contract_labels(g, lead, out);
+    free(lead);
+    return rc;
+}
 static int cmp_centry(const void* a, const void* b) {
     const centry* x = (const centry*)a; const centry* y = (const centry*)b;
     return (x->col > y->col) - (x->col < y->col);
 }
 
-/* contract g by mate[] into out; sets g->parent */
-static int contract_level(or_level* g, const int32_t* mate, or_level* out) {
+/* contract g by cluster labels (lead[u] in [0, n) names u's cluster) into
+ * out; coarse ids = rank of the distinct label values in ascending order (for
+ * the matching, lead = min(u, mate(u)): the rank of the cluster leader);
+ * sets g->parent */
+static int contract_labels(or_level* g, const int32_t* lead, or_level* out) {
     const int32_t n = g->n;
-    int32_t* cid = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int32_t* cid = (int32_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int32_t));
     g->parent = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
     if (!cid || !g->parent) { free(cid); return OR_ENOMEM; }
+    for (int32_t u = 0; u < n; ++u) cid[lead[u]] = 1; /* label used */
     int32_t nc = 0;
-    for (int32_t u = 0; u < n; ++u) {
-        const int32_t lead = (mate[u] >= 0 && mate[u] < u) ? mate[u] : u;
-        cid[u] = (lead == u) ? nc++ : -1;
-    }
-    for (int32_t u = 0; u < n; ++u) {
-        const int32_t lead = (mate[u] >= 0 && mate[u] < u) ? mate[u] : u;
-        g->parent[u] = cid[lead];
-    }
+    for (int32_t L = 0; L < n; ++L) cid[L] = cid[L] ? nc++ : -1;
+    for (int32_t u = 0; u < n; ++u) g->parent[u] = cid[lead[u]];
     free(cid);
     out->n = nc;
     out->c = (int64_t*)calloc((size_t)(nc > 0 ? nc : 1), sizeof(int64_t));
@@ -215,6 +224,71 @@ int or_build_hierarchy(int32_t n, const int64_t* rp, const int32_t* col,
         H->L += 1;
     }
     free(mate); free(cand);
+    *out = H;
+    return 0;
+}
+
+/* SCLaP hierarchy (reading R6): level h = 1, 2, ... uses
+ * U = max(max c, W), W = min(b^h, n0 / f); after a contraction that is not
+ * more than 10% smaller, f <- 0.7 f (the level is kept); stop at n <= n_stop,
+ * max_levels, or 10 consecutive ineffective decays, or when nothing merges. */
+int or_sclap_labels(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega, const int64_t* c,
+                    int64_t U, int32_t rounds, uint64_t seed, int32_t level, int32_t* lab);
+
+int or_build_hierarchy_sclap(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega,
+                             const int64_t* c, uint64_t seed, int32_t n_stop, int32_t max_levels, int32_t rounds,
+                             double f0, double b, or_hierarchy** out) {
+    if (n <= 0 || !rp || !col || !out || max_levels < 1 || rounds < 1 || !(f0 > 0.0) || !(b > 1.0)) return OR_EINVAL;
+    or_hierarchy* H = NULL;
+    /* level 0 via the matching builder with max_levels = 1 (copies the graph) */
+    int rc = or_build_hierarchy(n, rp, col, omega, c, seed, n, 1, 1, &H);
+    if (rc) return rc;
+    or_level* tmp = (or_level*)realloc(H->lv, sizeof(or_level) * (size_t)max_levels);
+    if (!tmp) { or_hier_free(H); return OR_ENOMEM; }
+    H->lv = tmp;
+    memset(H->lv + 1, 0, sizeof(or_level) * (size_t)(max_levels - 1));
+    int32_t* lab = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    if (!lab) { or_hier_free(H); return OR_ENOMEM; }
+    double f = f0;
+    int decays = 0;
+    while (H->L < max_levels) {
+        or_level* g = &H->lv[H->L - 1];
+        if (g->n <= n_stop) break;
+        const int32_t h = H->L; /* first coarsening uses h = 1 */
+        int64_t cmax = 0;
+        for (int32_t u = 0; u < g->n; ++u) if (g->c[u] > cmax) cmax = g->c[u];
+        double W = 1.0;
+        for (int32_t t = 0; t < h && W < 1e18; ++t) W *= b;
+        if ((double)n / f < W) W = (double)n / f;
+        const int64_t Wi = (int64_t)W; /* floor: cluster weights are integers */
+        const int64_t U = cmax > Wi ? cmax : Wi;
+        rc = or_sclap_labels(g->n, g->rp, g->col, g->omega, g->c, U, rounds, seed, h - 1, lab);
+        if (rc) break;
+        g->rounds = rounds;
+        or_level next;
+        memset(&next, 0, sizeof(next));
+        rc = contract_labels(g, lab, &next);
+        if (rc) { free(next.rp); free(next.col); free(next.omega); free(next.c); break; }
+        if (next.n == g->n) { /* nothing merged: stop, discard */
+            free(next.rp); free(next.col); free(next.omega); free(next.c);
+            free(g->parent);
+            g->parent = NULL;
+            if (++decays >= 10) break;
+            f *= 0.7;
+            continue;
+        }
+        if ((int64_t)10 * next.n > (int64_t)9 * g->n) {
+            f *= 0.7;
+            ++decays;
+        } else {
+            decays = 0;
+        }
+        H->lv[H->L] = next;
+        H->L += 1;
+        if (decays >= 10) break;
+    }
+    free(lab);
+    if (rc) { or_hier_free(H); return rc; }
     *out = H;
     return 0;
 }

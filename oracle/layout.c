@@ -15,6 +15,10 @@
 
 #include "mm_oracle.h"
 
+#ifndef M_PI
+#define M_PI 3.14159265358979323846
+#endif
+
 static double root_dim(double c, int dim) { return dim == 2 ? sqrt(c) : cbrt(c); }
 
 int or_coarse_sset(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col,
@@ -47,6 +51,33 @@ int or_prolong(int32_t n_fine, int dim, const int32_t* parent, const double* xc,
             const double U = or_uniform24(or_key_vertex(seed, OR_TAG_JITTER, (uint64_t)level, (uint64_t)u, dim, k));
             x[(int64_t)u * dim + k] = xc[(int64_t)parent[u] * dim + k] + 1e-3 * (2.0 * U - 1.0);
         }
+    return 0;
+}
+
+/* the paper's disc prolongation: "picking an angle uniformly at
+ * random in [0, 2pi] and a distance to P uniformly at random in [0, r]",
+ * r = sqrt(c(v')); dim 3 (extension): radius c^(1/3), direction from a
+ * uniform z in [-1, 1] and angle (reading R7). */
+int or_prolong_disc(int32_t n_fine, int dim, const int32_t* parent, const double* xc, const int64_t* c_coarse,
+                    uint64_t seed, int32_t level, double* x) {
+    if (n_fine < 0 || !parent || !xc || !x || !c_coarse) return OR_EINVAL;
+    for (int32_t u = 0; u < n_fine; ++u) {
+        const int32_t p = parent[u];
+        const double U0 = or_uniform24(or_key_vertex(seed, OR_TAG_DISC, (uint64_t)level, (uint64_t)u, 3, 0));
+        const double U1 = or_uniform24(or_key_vertex(seed, OR_TAG_DISC, (uint64_t)level, (uint64_t)u, 3, 1));
+        const double U2 = or_uniform24(or_key_vertex(seed, OR_TAG_DISC, (uint64_t)level, (uint64_t)u, 3, 2));
+        const double theta = 2.0 * M_PI * U0;
+        const double r = root_dim((double)c_coarse[p], dim) * U1;
+        if (dim == 2) {
+            x[(int64_t)u * 2 + 0] = xc[(int64_t)p * 2 + 0] + r * cos(theta);
+            x[(int64_t)u * 2 + 1] = xc[(int64_t)p * 2 + 1] + r * sin(theta);
+        } else {
+            const double z = 2.0 * U2 - 1.0, s = sqrt(1.0 - z * z);
+            x[(int64_t)u * 3 + 0] = xc[(int64_t)p * 3 + 0] + r * s * cos(theta);
+            x[(int64_t)u * 3 + 1] = xc[(int64_t)p * 3 + 1] + r * s * sin(theta);
+            x[(int64_t)u * 3 + 2] = xc[(int64_t)p * 3 + 2] + r * z;
+        }
+    }
     return 0;
 }
 

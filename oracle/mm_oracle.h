@@ -71,6 +71,12 @@ int or_build_hierarchy(int32_t n, const int64_t* rp, const int32_t* col,
                        const int64_t* omega /*NULL = unit*/, const int64_t* c /*NULL = unit*/,
                        uint64_t seed, int32_t n_stop, int32_t max_levels, int32_t max_rounds,
                        or_hierarchy** out);
+/* SCLaP hierarchy (reading R6 in sclap.c): rounds = l, f0 = 20, b = 2 */
+int or_build_hierarchy_sclap(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega,
+                             const int64_t* c, uint64_t seed, int32_t n_stop, int32_t max_levels, int32_t rounds,
+                             double f0, double b, or_hierarchy** out);
+int or_sclap_labels(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega, const int64_t* c,
+                    int64_t U, int32_t rounds, uint64_t seed, int32_t level, int32_t* lab);
 int32_t or_hier_num_levels(const or_hierarchy* h);
 /* level l graph sizes; arrays are owned by the hierarchy */
 int or_hier_level(const or_hierarchy* h, int32_t l, int32_t* n, int64_t* nnz,
@@ -110,6 +116,8 @@ int or_layout(int32_t n, int dim, const int64_t* rp, const int32_t* col,
  * else one level from x_init.  flags bit 1: dynamic update: start
  * at alpha_min on the finest level only, from x_init, with the hierarchy built
  * to at most h levels above the finest (the approximation level).
+ * flags bit 2: SCLaP hierarchy (R6; lp_rounds = 3, f = 20, b = 2) instead of the
+ * matching; bit 3: the paper's disc prolongation (R7) instead of Q15.
  * sweeps_out[l] = sweeps performed at level l (nullable, 64 entries). */
 typedef struct {
     double alpha0, alpha_min, factor, eps;
@@ -129,5 +137,8 @@ int or_full_stress(int32_t n, const int64_t* rp, const int32_t* col, int dim, co
 #define OR_TAG_INIT 0x494e4954ULL   /* "INIT" */
 #define OR_TAG_JITTER 0x4a495454ULL /* "JITT" */
 #define OR_TAG_MATCH 0x4d415443ULL  /* "MATC" */
+#define OR_TAG_DISC 0x44495343ULL   /* "DISC" */
+int or_prolong_disc(int32_t n_fine, int dim, const int32_t* parent, const double* xc, const int64_t* c_coarse,
+                    uint64_t seed, int32_t level, double* x);
 
 #endif

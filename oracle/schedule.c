@@ -81,7 +81,11 @@ int or_layout_schedule(int32_t n, int dim, const int64_t* rp, const int32_t* col
         or_hierarchy* H = NULL;
         /* dynamic: stop the coarsening after h levels (the approximation level) */
         const int32_t max_levels = dynamic ? (h + 1) : 64;
-        rc = or_build_hierarchy(n, rp, col, NULL, NULL, seed, dynamic ? 1 : n_stop, max_levels, 64, &H);
+        if (flags & 4)
+            rc = or_build_hierarchy_sclap(n, rp, col, NULL, NULL, seed, dynamic ? 1 : n_stop, max_levels, 3, 20.0, 2.0,
+                                          &H);
+        else
+            rc = or_build_hierarchy(n, rp, col, NULL, NULL, seed, dynamic ? 1 : n_stop, max_levels, 64, &H);
         if (rc) { free(xa); free(xb); return rc; }
         const int32_t nl = or_hier_num_levels(H), L = nl - 1;
         if (levels_out) *levels_out = nl;
@@ -135,7 +139,8 @@ int or_layout_schedule(int32_t n, int dim, const int64_t* rp, const int32_t* col
                 const int32_t nf = ln[l];
                 double* xf = (double*)malloc(sizeof(double) * (size_t)nf * dim);
                 double* xt = (double*)malloc(sizeof(double) * (size_t)nf * dim);
-                or_prolong(nf, dim, lpar[l], cur, seed, l, xf);
+                if (flags & 8) or_prolong_disc(nf, dim, lpar[l], cur, lc[l + 1], seed, l, xf);
+                else or_prolong(nf, dim, lpar[l], cur, seed, l, xf);
                 free(cur); free(tmp);
                 cur = xf; tmp = xt;
                 const int32_t hp = (h < L - l) ? h : (L - l);

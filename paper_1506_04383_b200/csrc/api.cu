@@ -18,6 +18,7 @@
 
 #include "k_fullstress.cuh"
 #include "k_hier.cuh"
+#include "k_sclap.cuh"
 #include "k_repulse.cuh"
 
 // ------------------------------------------------------------------ errors
@@ -556,8 +557,16 @@ T* alloc_n(size_t count, cudaStream_t st) {
     return (T*)dev_alloc(sizeof(T) * (count > 0 ? count : 1), st);
 }
 
+// clustering of the hierarchy: heavy-edge matching (Q16, default) or SCLaP (R6)
+struct HierMode {
+    bool sclap = false;
+    int32_t lp_rounds = 3;
+    double f0 = 20.0, b = 2.0;
+};
+
 mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uint64_t seed, int32_t n_stop,
-                               int32_t max_levels, int32_t max_rounds, mm_hierarchy** out, cudaStream_t st) {
+                               int32_t max_levels, int32_t max_rounds, mm_hierarchy** out, cudaStream_t st,
+                               const HierMode& mode = HierMode()) {
     const int32_t n0 = g->n;
     const int64_t nnz0 = g->nnz;
     mm_hierarchy* H = new mm_hierarchy();
@@ -602,15 +611,15 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
     // scratch sized by level 0 (levels only shrink)
     const int64_t m0 = std::max<int64_t>(nnz0, 1);
     const size_t tmpb = std::max(sort_temp_bytes_u64(m0), scan_temp_bytes((int32_t)std::max<int64_t>(m0, n0 + 2))) + 256;
-    const size_t bytes = al((size_t)n0 * 4) * 6 + al(64) + al((size_t)m0 * 8) * 2 + al((size_t)m0 * 4) * 6 +
+    const size_t bytes = al((size_t)n0 * 4 + 8) * 6 + al(64) + al((size_t)m0 * 8) * 2 + al((size_t)m0 * 4) * 6 +
                          al(((size_t)n0 + 2) * 4) * 2 + al(tmpb) + 4096;
     DevBuf scratch(bytes, st);
     if (!scratch.p) { set_err("mm_build_hierarchy: out of memory (%zu B scratch)", bytes); return fail(MM_ERR_OUT_OF_MEMORY); }
     Carver cv(scratch.p, bytes);
     int32_t* mate = cv.take<int32_t>(n0);
-    int32_t* cand = cv.take<int32_t>(n0);
-    int32_t* flag = cv.take<int32_t>(n0);
-    int32_t* cid = cv.take<int32_t>(n0);
+    int32_t* cand = cv.take<int32_t>(n0);  // SCLaP: the labels
+    int32_t* flag = cv.take<int32_t>((size_t)n0 + 2);
+    int32_t* cid = cv.take<int32_t>((size_t)n0 + 2);
     int32_t* cnext = cv.take<int32_t>(n0);
     int32_t* spare = cv.take<int32_t>(n0);
     (void)spare;
@@ -628,10 +637,56 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
     void* tmp = cv.take<char>(tmpb);
     if (!cv.ok) { set_err("mm_build_hierarchy: scratch carving failed"); return fail(MM_ERR_INVALID_ARGUMENT); }
 
+    double f = mode.f0;
+    int decays = 0;
     while ((int32_t)H->lv.size() < max_levels) {
         const size_t li = H->lv.size() - 1;
         const HLevel cur = H->lv[li];
         if (cur.n <= n_stop) break;
+        int32_t nc = 0;
+        int32_t* parent = nullptr;
+        if (mode.sclap) {
+            // U = max(max c, W), W = min(b^h, n0 / f), h = 1 for the first coarsening
+            const int32_t h = (int32_t)li + 1;
+            int32_t cmax = 0;
+            if (launch_max_i32(cur.n, cur.c, added, st) || cudaMemcpyAsync(&cmax, added, 4, cudaMemcpyDeviceToHost, st) ||
+                cudaStreamSynchronize(st)) {
+                set_err("mm_build_hierarchy: max c failed");
+                return fail(MM_ERR_CUDA);
+            }
+            double W = 1.0;
+            for (int32_t t = 0; t < h && W < 1e18; ++t) W *= mode.b;
+            W = std::min(W, (double)n0 / f);
+            const long long U = std::max<long long>(cmax, (long long)W);
+            int32_t used = 0;
+            cudaError_t e = sclap_labels_gpu(cur.n, cur.nnz, cur.rp, cur.col, cur.omega, cur.c, U, mode.lp_rounds,
+                                             seed, (int32_t)li, cand, &used, st, dev_alloc, dev_free);
+            if (e != cudaSuccess) {
+                set_err("mm_build_hierarchy: SCLaP failed: %s", cudaGetErrorString(e));
+                return fail(e == cudaErrorMemoryAllocation ? MM_ERR_OUT_OF_MEMORY : MM_ERR_CUDA);
+            }
+            H->lv[li].rounds = mode.lp_rounds;
+            parent = alloc_n<int32_t>(cur.n, st);
+            if (!parent) { set_err("mm_build_hierarchy: out of memory"); return fail(MM_ERR_OUT_OF_MEMORY); }
+            if (contract_labels_gpu(cur.n, cand, cur.c, flag, cid, parent, cnext, added, tmp, tmpb, st) ||
+                cudaMemcpyAsync(&nc, added, 4, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st)) {
+                dev_free(parent, st);
+                set_err("mm_build_hierarchy: label contraction failed: %s", cudaGetErrorString(cudaGetLastError()));
+                return fail(MM_ERR_CUDA);
+            }
+            if (nc == cur.n) {  // nothing merged: decay f and retry this level (at most 10 times)
+                dev_free(parent, st);
+                f *= 0.7;
+                if (++decays >= 10) break;
+                continue;
+            }
+            if ((int64_t)10 * nc > (int64_t)9 * cur.n) {  // "not more than 10% smaller": f <- 0.7 f
+                f *= 0.7;
+                ++decays;
+            } else {
+                decays = 0;
+            }
+        } else {
         if (launch_fill(cur.n, -1, mate, st) != cudaSuccess) { set_err("mm_build_hierarchy: fill"); return fail(MM_ERR_CUDA); }
         int32_t rounds = max_rounds;
         for (int32_t r = 0; r < max_rounds; ++r) {
@@ -649,7 +704,7 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
             }
         }
         H->lv[li].rounds = rounds;
-        int32_t* parent = alloc_n<int32_t>(cur.n, st);
+        parent = alloc_n<int32_t>(cur.n, st);
         if (!parent) { set_err("mm_build_hierarchy: out of memory"); return fail(MM_ERR_OUT_OF_MEMORY); }
         int32_t last[2] = {0, 0};
         if (contract_leaders(cur.n, mate, cur.c, flag, cid, parent, cnext, tmp, tmpb, st) ||
@@ -659,10 +714,11 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
             set_err("mm_build_hierarchy: contraction failed: %s", cudaGetErrorString(cudaGetLastError()));
             return fail(MM_ERR_CUDA);
         }
-        const int32_t nc = last[0] + last[1];
+        nc = last[0] + last[1];
         if ((int64_t)10 * nc > (int64_t)9 * cur.n) {  // Q17: less than 10% smaller -> discard, stop
             dev_free(parent, st);
             break;
+        }
         }
         int64_t m2 = 0;
         if (cur.nnz > 0) {
@@ -701,6 +757,7 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
             set_err("mm_build_hierarchy: level assembly failed: %s", cudaGetErrorString(cudaGetLastError()));
             return fail(MM_ERR_CUDA);
         }
+        if (mode.sclap && decays >= 10) break;
     }
     if (cudaStreamSynchronize(st) != cudaSuccess) {
         set_err("mm_build_hierarchy: %s", cudaGetErrorString(cudaGetLastError()));
@@ -735,6 +792,27 @@ mm_status mm_build_hierarchy(const mm_graph* g, const int32_t* c, int dim, uint6
     }
     *out = nullptr;
     return build_hierarchy_impl(g, c, dim, seed, n_stop, max_levels, max_rounds, out, (cudaStream_t)stream);
+}
+
+mm_status mm_build_hierarchy_sclap(const mm_graph* g, const int32_t* c, int dim, uint64_t seed, int32_t n_stop,
+                                   int32_t max_levels, int32_t lp_rounds, double f0, double b, mm_hierarchy** out,
+                                   mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_graph(g, "mm_build_hierarchy_sclap")) != MM_OK) return s;
+    if (dim != 2 && dim != 3) { set_err("mm_build_hierarchy_sclap: dim must be 2 or 3"); return MM_ERR_UNSUPPORTED; }
+    if (!out || n_stop < 1 || max_levels < 1 || max_levels > MM_MAX_LEVELS || lp_rounds < 1 || !(f0 > 0.0) ||
+        !(b > 1.0)) {
+        set_err("mm_build_hierarchy_sclap: bad arguments (out, n_stop >= 1, 1 <= max_levels <= %d, lp_rounds >= 1, "
+                "f0 > 0, b > 1)", MM_MAX_LEVELS);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    *out = nullptr;
+    HierMode m;
+    m.sclap = true;
+    m.lp_rounds = lp_rounds;
+    m.f0 = f0;
+    m.b = b;
+    return build_hierarchy_impl(g, c, dim, seed, n_stop, max_levels, 64, out, (cudaStream_t)stream, m);
 }
 
 int32_t mm_hierarchy_num_levels(const mm_hierarchy* h) { return h ? (int32_t)h->lv.size() : 0; }
@@ -1059,7 +1137,10 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
         mm_hierarchy* H = nullptr;
         // dynamic update: "stop the coarsening process after the computation of h levels"
         const int32_t max_levels = dynamic ? std::min(h + 1, (int)MM_MAX_LEVELS) : MM_MAX_LEVELS;
-        if ((s = build_hierarchy_impl(g, nullptr, dim, seed, dynamic ? 1 : n_stop, max_levels, 64, &H, ls)) != MM_OK)
+        HierMode hm;
+        hm.sclap = (flags & MM_LAYOUT_SCLAP) != 0;
+        if ((s = build_hierarchy_impl(g, nullptr, dim, seed, dynamic ? 1 : n_stop, max_levels, 64, &H, ls, hm)) !=
+            MM_OK)
             return s;
         struct HGuard {
             mm_hierarchy* h;
@@ -1112,7 +1193,11 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
             const int32_t nf = H->lv[l].n;
             if (!dynamic && l < L) {
                 float* dst = (cur == xa) ? xb : xa;
-                MM_CU(launch_prolong(dim, nf, H->lv[l].parent, cur, seed, l, dst, ls), "mm_layout prolong");
+                if (flags & MM_LAYOUT_DISC_PROLONG)
+                    MM_CU(launch_prolong_disc(dim, nf, H->lv[l].parent, cur, H->lv[l + 1].c, seed, l, dst, ls),
+                          "mm_layout prolong");
+                else
+                    MM_CU(launch_prolong(dim, nf, H->lv[l].parent, cur, seed, l, dst, ls), "mm_layout prolong");
                 cur = dst;
             }
             const int32_t hp = std::min(h, L - l);
@@ -1217,7 +1302,7 @@ extern "C" mm_status mm_layout_schedule(const mm_graph* g, const mm_sset* S, int
     if ((s = check_x(x_out, dim, "x_out", who)) != MM_OK) return s;
     if (!sch || h < 0 || sch->a < 1 || sch->max_final_iters < 1 || !(sch->alpha_min > 0.0) ||
         !(sch->alpha0 >= sch->alpha_min) || !(sch->factor > 0.0 && sch->factor < 1.0) || !(sch->eps >= 0.0) ||
-        (flags & ~(MM_LAYOUT_MULTILEVEL | MM_LAYOUT_DYNAMIC)) != 0) {
+        (flags & ~(MM_LAYOUT_MULTILEVEL | MM_LAYOUT_DYNAMIC | MM_LAYOUT_SCLAP | MM_LAYOUT_DISC_PROLONG)) != 0) {
         set_err("%s: bad arguments (schedule: a >= 1, max_final_iters >= 1, 0 < alpha_min <= alpha0, "
                 "0 < factor < 1, eps >= 0; h >= 0; flags)", who);
         return MM_ERR_INVALID_ARGUMENT;

@@ -257,6 +257,54 @@ __global__ void k_init_box(int32_t n, const double* __restrict__ dsum, int64_t n
     store_x<DIM>(x, u, make_float4(o[0], o[1], DIM == 3 ? o[2] : 0.f, 0.f));
 }
 
+// ---- label-based contraction (SCLaP, R6): coarse id = rank of the distinct labels
+__global__ void k_label_flags(int32_t n, const int32_t* __restrict__ lab, int32_t* __restrict__ flag) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u < n) flag[lab[u]] = 1;  // benign race: every writer stores 1
+}
+__global__ void k_label_parent(int32_t n, const int32_t* __restrict__ lab, const int32_t* __restrict__ cid,
+                               const int32_t* __restrict__ c, int32_t* __restrict__ parent,
+                               int32_t* __restrict__ c_next) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int32_t p = cid[lab[u]];
+    parent[u] = p;
+    atomicAdd(c_next + p, c[u]);  // integer: order-free
+}
+
+// the paper's disc prolongation (reading R7): angle U0 * 2pi, radius
+// c(v')^(1/dim) * U1; dim 3 direction from z = 2 U2 - 1
+template <int DIM>
+__global__ void k_prolong_disc(int32_t n, const int32_t* __restrict__ parent, const float* __restrict__ xc,
+                               const int32_t* __restrict__ c_coarse, uint64_t seed, int32_t level,
+                               float* __restrict__ x) {
+    const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
+    if (u >= n) return;
+    const int32_t p = parent[u];
+    const float4 pc = load_x<DIM>(xc, p);
+    const uint64_t k0 = mix64(mix64(seed ^ kTagDisc) ^ (uint64_t)level);
+    const float U0 = uniform24(mix64(k0 ^ ((uint64_t)u * 3 + 0)));
+    const float U1 = uniform24(mix64(k0 ^ ((uint64_t)u * 3 + 1)));
+    const float U2 = uniform24(mix64(k0 ^ ((uint64_t)u * 3 + 2)));
+    const float cp = (float)c_coarse[p];
+    const float r = (DIM == 2 ? sqrtf(cp) : cbrtf(cp)) * U1;
+    float sn, cs;
+    sincosf(6.28318530717958647692f * U0, &sn, &cs);
+    if (DIM == 2) {
+        store_x<DIM>(x, u, make_float4(pc.x + r * cs, pc.y + r * sn, 0.f, 0.f));
+    } else {
+        const float z = 2.0f * U2 - 1.0f, sz = sqrtf(fmaxf(0.f, 1.0f - z * z));
+        store_x<DIM>(x, u, make_float4(pc.x + r * sz * cs, pc.y + r * sz * sn, pc.z + r * z, 0.f));
+    }
+}
+
+__global__ void k_max_i32(int32_t n, const int32_t* __restrict__ a, int32_t* __restrict__ out) {
+    int32_t m = 0;
+    for (int32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) m = max(m, a[t]);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
 // FP64 sum of a float array (one block, fixed order)
 __global__ void k_sum_f32(int64_t m, const float* __restrict__ a, double* __restrict__ out) {
     __shared__ double red[32];
@@ -438,6 +486,47 @@ cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, dou
     LaunchScope ls("init_box", st);
     if (dim == 2) k_init_box<2><<<nblk(n), 256, 0, st>>>(n, dsum, nnz, seed, level, x);
     else k_init_box<3><<<nblk(n), 256, 0, st>>>(n, dsum, nnz, seed, level, x);
+    return cudaGetLastError();
+}
+
+}  // namespace mm
+
+namespace mm {
+
+cudaError_t contract_labels_gpu(int32_t n, const int32_t* lab, const int32_t* c, int32_t* flag, int32_t* cid,
+                                int32_t* parent, int32_t* c_next, int32_t* nc_out_dev, void* tmp, size_t tmp_bytes,
+                                cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(flag, 0, sizeof(int32_t) * ((size_t)n + 1), st);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope ls("label_flags", st);
+        k_label_flags<<<nblk(n), 256, 0, st>>>(n, lab, flag);
+    }
+    // exclusive scan over n + 1 entries: cid[n] = number of clusters
+    e = exclusive_scan_i32(flag, cid, n + 1, tmp, tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    e = cudaMemsetAsync(c_next, 0, sizeof(int32_t) * (size_t)n, st);
+    if (e != cudaSuccess) return e;
+    {
+        LaunchScope ls("label_parent", st);
+        k_label_parent<<<nblk(n), 256, 0, st>>>(n, lab, cid, c, parent, c_next);
+    }
+    return cudaMemcpyAsync(nc_out_dev, cid + n, sizeof(int32_t), cudaMemcpyDeviceToDevice, st);
+}
+
+cudaError_t launch_prolong_disc(int dim, int32_t n, const int32_t* parent, const float* xc, const int32_t* c_coarse,
+                                uint64_t seed, int32_t level, float* x, cudaStream_t st) {
+    LaunchScope ls("prolong_disc", st);
+    if (dim == 2) k_prolong_disc<2><<<nblk(n), 256, 0, st>>>(n, parent, xc, c_coarse, seed, level, x);
+    else k_prolong_disc<3><<<nblk(n), 256, 0, st>>>(n, parent, xc, c_coarse, seed, level, x);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_max_i32(int32_t n, const int32_t* a, int32_t* out, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(out, 0, sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    LaunchScope ls("max_c", st);
+    k_max_i32<<<std::max(1, std::min(nblk(n), 1184)), 256, 0, st>>>(n, a, out);
     return cudaGetLastError();
 }
 

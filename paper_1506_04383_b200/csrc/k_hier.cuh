@@ -34,4 +34,11 @@ cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const floa
 cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,
                             int32_t level, float* x, cudaStream_t st);
 
+// SCLaP (R6): labels -> parent map, coarse weights; *nc_out_dev = number of clusters
+cudaError_t contract_labels_gpu(int32_t n, const int32_t* lab, const int32_t* c, int32_t* flag, int32_t* cid,
+                                int32_t* parent, int32_t* c_next, int32_t* nc_out_dev, void* tmp, size_t tmp_bytes,
+                                cudaStream_t st);
+cudaError_t launch_prolong_disc(int dim, int32_t n, const int32_t* parent, const float* xc, const int32_t* c_coarse,
+                                uint64_t seed, int32_t level, float* x, cudaStream_t st);
+cudaError_t launch_max_i32(int32_t n, const int32_t* a, int32_t* out, cudaStream_t st);
 }  // namespace mm

@@ -96,6 +96,7 @@ __host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
 constexpr uint64_t kTagInit = 0x494e4954ULL;    // "INIT"
 constexpr uint64_t kTagJitter = 0x4a495454ULL;  // "JITT"
 constexpr uint64_t kTagMatch = 0x4d415443ULL;   // "MATC"
+constexpr uint64_t kTagDisc = 0x44495343ULL;    // "DISC"
 
 __device__ __forceinline__ float uniform24(uint64_t key) {
     return (float)(uint32_t)(key >> 40) * (1.0f / 16777216.0f);

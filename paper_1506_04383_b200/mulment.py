@@ -22,7 +22,7 @@ MM_ERR_OUT_OF_MEMORY, MM_ERR_CUDA, MM_ERR_UNSUPPORTED = -4, -5, -6
 MM_MAX_LEVELS = 64
 
 EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator", "mm_sweep_workspace",
-           "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_hierarchy_num_levels", "mm_hierarchy_level",
+           "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_build_hierarchy_sclap", "mm_hierarchy_num_levels", "mm_hierarchy_level",
            "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_full_stress",
            "mm_launch_count",
            "mm_profile_enable",
@@ -75,7 +75,7 @@ class mm_schedule(ctypes.Structure):
                 ("eps", ctypes.c_double), ("a", ctypes.c_int32), ("max_final_iters", ctypes.c_int32)]
 
 
-MM_LAYOUT_MULTILEVEL, MM_LAYOUT_DYNAMIC = 1, 2
+MM_LAYOUT_MULTILEVEL, MM_LAYOUT_DYNAMIC, MM_LAYOUT_SCLAP, MM_LAYOUT_DISC_PROLONG = 1, 2, 4, 8
 
 
 def paper_schedule(**kw) -> mm_schedule:
@@ -115,6 +115,8 @@ def load() -> ctypes.CDLL:
     L.mm_energy.restype = ctypes.c_int
     L.mm_build_hierarchy.argtypes = [P(mm_graph), vp, ctypes.c_int, u64, i32, i32, i32, P(vp), vp]
     L.mm_build_hierarchy.restype = ctypes.c_int
+    L.mm_build_hierarchy_sclap.argtypes = [P(mm_graph), vp, ctypes.c_int, u64, i32, i32, i32, f64, f64, P(vp), vp]
+    L.mm_build_hierarchy_sclap.restype = ctypes.c_int
     L.mm_hierarchy_num_levels.argtypes = [vp]; L.mm_hierarchy_num_levels.restype = i32
     L.mm_hierarchy_level.argtypes = [vp, i32, P(mm_level_view)]; L.mm_hierarchy_level.restype = ctypes.c_int
     L.mm_hierarchy_free.argtypes = [vp]; L.mm_hierarchy_free.restype = None
@@ -311,13 +313,19 @@ class Hierarchy:
 
 
 def build_hierarchy(g: DeviceGraph, dim: int, seed: int, n_stop: int = 1000, max_levels: int = 64,
-                    max_rounds: int = 64, c=None) -> Hierarchy:
+                    max_rounds: int = 64, c=None, sclap: bool = False, lp_rounds: int = 3, f0: float = 20.0,
+                    b: float = 2.0) -> Hierarchy:
     L = load()
     h = ctypes.c_void_p()
     gs = g.c_struct()
-    rc = L.mm_build_hierarchy(ctypes.byref(gs), _ptr(c), dim, seed, n_stop, max_levels, max_rounds,
-                              ctypes.byref(h), _stream_ptr(g.row_ptr.device))
-    _check(rc, "mm_build_hierarchy")
+    if sclap:
+        rc = L.mm_build_hierarchy_sclap(ctypes.byref(gs), _ptr(c), dim, seed, n_stop, max_levels, lp_rounds, f0, b,
+                                        ctypes.byref(h), _stream_ptr(g.row_ptr.device))
+        _check(rc, "mm_build_hierarchy_sclap")
+    else:
+        rc = L.mm_build_hierarchy(ctypes.byref(gs), _ptr(c), dim, seed, n_stop, max_levels, max_rounds,
+                                  ctypes.byref(h), _stream_ptr(g.row_ptr.device))
+        _check(rc, "mm_build_hierarchy")
     return Hierarchy(h.value)
 
 
@@ -352,7 +360,7 @@ def _report(rep: mm_layout_report) -> dict:
 
 def layout_schedule(g: Optional[DeviceGraph], S: DeviceSSet, dim: int, q: float, h: int, sched: mm_schedule,
                     seed: int, n_stop: int = 1000, multilevel: bool = True, dynamic: bool = False, x_init=None,
-                    out=None):
+                    out=None, sclap: bool = False, disc: bool = False):
     """The paper's alpha schedule or the dynamic update.
     Returns (x_out tensor, report dict incl. sweeps_level)."""
     torch = _torch()
@@ -364,7 +372,8 @@ def layout_schedule(g: Optional[DeviceGraph], S: DeviceSSet, dim: int, q: float,
     rep = mm_layout_report()
     gs = g.c_struct() if g is not None else None
     s = S.c_struct()
-    flags = (MM_LAYOUT_MULTILEVEL if multilevel else 0) | (MM_LAYOUT_DYNAMIC if dynamic else 0)
+    flags = ((MM_LAYOUT_MULTILEVEL if multilevel else 0) | (MM_LAYOUT_DYNAMIC if dynamic else 0) |
+             (MM_LAYOUT_SCLAP if sclap else 0) | (MM_LAYOUT_DISC_PROLONG if disc else 0))
     rc = L.mm_layout_schedule(ctypes.byref(gs) if gs is not None else None, ctypes.byref(s), dim, float(q), int(h),
                               ctypes.byref(sched), int(seed), int(n_stop), flags, _ptr(x_init), _ptr(out),
                               ctypes.byref(rep), _stream_ptr(device))

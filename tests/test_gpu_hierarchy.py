@@ -68,3 +68,24 @@ def test_hierarchy_with_weights(mm):
     for l in range(len(want) - 1):
         assert np.array_equal(H.level_host(l)["parent"], want[l].parent)
         assert np.array_equal(H.level_host(l + 1)["omega"].astype(np.int64), want[l + 1].omega)
+
+
+@pytest.mark.parametrize("name", ["cfg3_mesh64", "cfg5_grid16", "cfg4_cl20000", "cfg3", "cfg4"])
+def test_sclap_hierarchy_bitwise(mm, name):
+    """SCLaP (R6) on the GPU vs the oracle: every level identical."""
+    import oracle
+
+    w = workload(name)
+    n_stop = 1000 if w.n > 50000 else 100
+    lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=n_stop, sclap=True)
+    H = mm.build_hierarchy(mm.graph_to_device(w.graph), w.dim, w.seed, n_stop=n_stop, sclap=True)
+    assert H.num_levels == len(lv), (H.num_levels, [l.n for l in lv])
+    for l, ol in enumerate(lv):
+        gl = H.level_host(l)
+        assert gl["n"] == ol.n, l
+        assert np.array_equal(gl["row_ptr"], ol.row_ptr), l
+        assert np.array_equal(gl["col"], ol.col), l
+        assert np.array_equal(gl["omega"].astype(np.int64), ol.omega), l
+        assert np.array_equal(gl["c"].astype(np.int64), ol.c), l
+        if l < len(lv) - 1:
+            assert np.array_equal(gl["parent"], ol.parent), l

@@ -81,3 +81,25 @@ def test_dynamic_update(mm):
     assert rep["levels"] == nl == 3
     assert rep["sweeps_level"] == list(sw), (rep["sweeps_level"], list(sw))
     assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep["energy"], eo)
+
+
+@pytest.mark.parametrize("name,dim", [("cfg3_mesh64", 2), ("cfg5_grid12", 3)])
+def test_schedule_sclap_disc(mm, name, dim):
+    """The paper's configuration end to end: SCLaP hierarchy (R6), disc
+    prolongation (R7), alpha schedule, h = 2."""
+    w = workload(name)
+    gs, os_ = _sched(mm, 20)
+    x, rep = mm.layout_schedule(mm.graph_to_device(w.graph), mm.sset_to_device(w.S), w.dim, w.q, 2, gs, w.seed,
+                                n_stop=100, sclap=True, disc=True)
+    xo, eo, nl, sw = oracle.layout_schedule(w.graph, w.S, w.dim, w.q, 2, os_, w.seed, n_stop=100, sclap=True, disc=True)
+    assert rep["levels"] == nl
+    eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), 0.008, w.q)
+    assert _rel(rep["energy"], eg[2]) <= 1e-4
+    assert rep["sweeps_level"] == list(sw), (rep["sweeps_level"], list(sw))
+
+    def control(s):
+        ps = oracle.paper_schedule(max_final_iters=20, alpha0=1.0 * (1 + s), alpha_min=0.008 * (1 + s))
+        return oracle.layout_schedule(w.graph, w.S, w.dim, w.q, 2, ps, w.seed, n_stop=100, sclap=True,
+                                      disc=True)[1][2]
+
+    assert_energy_or_chaos(rep["energy"], eo[2], control, f"{name} sclap+disc")

@@ -156,3 +156,49 @@ def test_layout_multilevel_small_runs():
     # the finest-level result is a pure function of the seed
     x2, e2, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 2, [4], w.seed, n_stop=100)
     np.testing.assert_array_equal(x, x2)
+
+
+# ---------------------------------------------------------------- SCLaP (f2, reading R6)
+@pytest.mark.parametrize("name", ["cfg3_mesh64", "cfg5_grid16", "cfg4_cl20000"])
+def test_sclap_hierarchy_invariants(name):
+    """Cluster weights respect U = max(max c, min(2^h, n/f)); weights conserved;
+    contraction = Pm^T A Pm; coarse ids rank the distinct labels."""
+    w = configs.make(name)
+    lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=100, sclap=True)
+    assert len(lv) >= 3
+    f = 20.0
+    for l in range(len(lv) - 1):
+        fine, coarse = lv[l], lv[l + 1]
+        P = fine.parent
+        k = coarse.n
+        np.testing.assert_array_equal(np.bincount(P, weights=fine.c, minlength=k).astype(np.int64), coarse.c)
+        W = min(2.0 ** (l + 1), w.n / f)
+        U = max(int(fine.c.max()), int(W))
+        assert coarse.c.max() <= U, (l, coarse.c.max(), U)
+        n = fine.n
+        A = sp.csr_matrix((fine.omega.astype(np.float64), fine.col, fine.row_ptr), shape=(n, n))
+        Pm = sp.csr_matrix((np.ones(n), (np.arange(n), P)), shape=(n, k))
+        C = (Pm.T @ A @ Pm).tocsr()
+        C.setdiag(0)
+        C.eliminate_zeros()
+        C.sort_indices()
+        np.testing.assert_array_equal(C.indptr, coarse.row_ptr)
+        np.testing.assert_array_equal(C.indices, coarse.col)
+        if 10 * coarse.n > 9 * fine.n:
+            f *= 0.7
+
+
+def test_sclap_triangle_single_cluster():
+    """Triangle, U = 3: node 1 joins label 0; node 2 joins 0 or 1 (hash tie);
+    the next round moves everything into label 0 (re-derived for R6)."""
+    g = graphs.from_edges(3, np.array([0, 0, 1]), np.array([1, 2, 2]))
+    lab = oracle.sclap_labels(g, U=3, rounds=3, seed=42, level=0)
+    assert lab.tolist() == [0, 0, 0]
+
+
+def test_sclap_size_bound_blocks_merge():
+    """Path 0-1-2-3 with U = 2: every accepted cluster weighs <= 2."""
+    g = H.path(4)
+    lab = oracle.sclap_labels(g, U=2, rounds=5, seed=1, level=0)
+    assert np.bincount(lab).max() <= 2
+    assert lab[1] == 0  # node 1 moves to the smaller label 0 in round 0
