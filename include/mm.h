@@ -156,6 +156,13 @@ MM_API const char* mm_version(void);
 MM_API mm_status mm_set_allocator(void* (*alloc)(size_t, mm_stream_t, void*),
                            void (*free_)(void*, mm_stream_t, void*), void* ctx);
 
+/* Validate an S set on the device (syncs): row_ptr monotone within [0, nnz],
+ * 0 <= col < n, no self entry, d > 0 finite, w >= 0 finite, rho_i > 0 for every
+ * row (P:106 connected graphs; reading Q22).  Returns MM_ERR_INVALID_INPUT with
+ * the first offending row and the reasons in mm_last_error().  Duplicate
+ * entries are not detected.  The sweep entry points do not validate (cost). */
+MM_API mm_status mm_validate_sset(const mm_sset* S, mm_stream_t stream);
+
 /* Scratch bytes mm_sweep needs for n vertices (host out). ap = NULL: exact. */
 MM_API mm_status mm_sweep_workspace(int32_t n, int dim, const mm_approx* ap, size_t* bytes);
 

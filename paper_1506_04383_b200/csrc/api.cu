@@ -1359,3 +1359,23 @@ extern "C" mm_status mm_full_stress(const mm_graph* g, int dim, const float* x, 
     out[3] = P;
     return MM_OK;
 }
+
+// ================================================================== validation
+extern "C" mm_status mm_validate_sset(const mm_sset* S, mm_stream_t stream) {
+    mm_status s;
+    if ((s = check_sset(S, "mm_validate_sset")) != MM_OK) return s;
+    cudaStream_t st = (cudaStream_t)stream;
+    DevBuf buf(64, st);
+    if (!buf.p) { set_err("mm_validate_sset: out of device memory"); return MM_ERR_OUT_OF_MEMORY; }
+    int32_t init[2] = {INT32_MAX, 0}, h[2] = {0, 0};
+    MM_CU(cudaMemcpyAsync(buf.p, init, 8, cudaMemcpyHostToDevice, st), "mm_validate_sset h2d");
+    MM_CU(launch_validate_sset(S->n, S->row_ptr, S->col, S->d, S->w, S->nnz, (int32_t*)buf.p, st), "mm_validate_sset");
+    MM_CU(cudaMemcpyAsync(h, buf.p, 8, cudaMemcpyDeviceToHost, st), "mm_validate_sset d2h");
+    MM_CU(cudaStreamSynchronize(st), "mm_validate_sset sync");
+    if (h[1] == 0) return MM_OK;
+    set_err("mm_validate_sset: row %d is invalid (%s%s%s%s%s%s)", h[0] - 1, (h[1] & 1) ? "row_ptr not monotone; " : "",
+            (h[1] & 2) ? "col out of range; " : "", (h[1] & 4) ? "self entry; " : "",
+            (h[1] & 8) ? "d <= 0 or non-finite; " : "", (h[1] & 16) ? "w < 0 or non-finite; " : "",
+            (h[1] & 32) ? "rho_i <= 0" : "");
+    return MM_ERR_INVALID_INPUT;
+}

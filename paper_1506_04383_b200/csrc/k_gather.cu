@@ -394,3 +394,43 @@ cudaError_t launch_energy_s(int dim, double q, int32_t n, const int64_t* rp, con
 }
 
 }  // namespace mm
+
+namespace mm {
+namespace {
+// S-set validation: per row i, row_ptr monotone, 0 <= col < n, col != i,
+// d > 0 finite, w >= 0 finite, rho_i = sum w > 0.  bad[0] = first bad row + 1
+// (atomicMin on a 1-based row, 0 = none), bad[1] = OR of the reason bits.
+__global__ void k_validate_sset(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+                                const float* __restrict__ d, const float* __restrict__ w, int64_t nnz,
+                                int32_t* __restrict__ bad) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int reason = 0;
+    const int64_t b = rp[i], e = rp[i + 1];
+    if (b < 0 || e < b || e > nnz) reason |= 1;
+    double rho = 0.0;
+    if (!(reason & 1)) {
+        for (int64_t t = b; t < e; ++t) {
+            const int32_t j = col[t];
+            if (j < 0 || j >= n) reason |= 2;
+            if (j == i) reason |= 4;
+            if (!(d[t] > 0.f) || !isfinite(d[t])) reason |= 8;
+            if (!(w[t] >= 0.f) || !isfinite(w[t])) reason |= 16;
+            rho += w[t];
+        }
+        if (!(rho > 0.0)) reason |= 32;
+    }
+    if (reason) {
+        atomicMin(bad, i + 1);
+        atomicOr(bad + 1, reason);
+    }
+}
+}  // namespace
+
+cudaError_t launch_validate_sset(int32_t n, const int64_t* rp, const int32_t* col, const float* d, const float* w,
+                                 int64_t nnz, int32_t* bad, cudaStream_t st) {
+    LaunchScope ls("validate_sset", st);
+    k_validate_sset<<<(n + 255) / 256, 256, 0, st>>>(n, rp, col, d, w, nnz, bad);
+    return cudaGetLastError();
+}
+}  // namespace mm

@@ -50,7 +50,7 @@ __device__ __forceinline__ f2x inv_pair(f2x r2, float cexp) {
     }
 }
 
-template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1>
+template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4>
 __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
                                                     const float4* __restrict__ rep_hi,
                                                     const float4* __restrict__ rep_lo,
@@ -116,7 +116,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             f2x TX[G], TY[G], TZ[G];
 #pragma unroll
             for (int gg = 0; gg < G; ++gg) TX[gg] = TY[gg] = TZ[gg] = 0ull;
-#pragma unroll 4
+#pragma unroll UNR
             for (int jj = 0; jj < cnt; ++jj) {
                 float sx, sy, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f, nu = 1.f;
                 if constexpr (COARSE) {

@@ -80,4 +80,6 @@ cudaError_t launch_energy_s(int dim, double q, int32_t n, const int64_t* rp, con
                             const float* w, const float* x, double mean_row, double* partial, int32_t* coinc,
                             cudaStream_t st);
 
+cudaError_t launch_validate_sset(int32_t n, const int64_t* rp, const int32_t* col, const float* d, const float* w,
+                                 int64_t nnz, int32_t* bad, cudaStream_t st);
 }  // namespace mm

@@ -21,7 +21,8 @@ MM_OK, MM_ERR_INVALID_ARGUMENT, MM_ERR_INVALID_INPUT, MM_ERR_NONFINITE = 0, -1, 
 MM_ERR_OUT_OF_MEMORY, MM_ERR_CUDA, MM_ERR_UNSUPPORTED = -4, -5, -6
 MM_MAX_LEVELS = 64
 
-EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator", "mm_sweep_workspace",
+EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator", "mm_validate_sset",
+           "mm_sweep_workspace",
            "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_build_hierarchy_sclap", "mm_hierarchy_num_levels", "mm_hierarchy_level",
            "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_full_stress",
            "mm_launch_count",
@@ -107,6 +108,7 @@ def load() -> ctypes.CDLL:
     L.mm_last_error.argtypes = []; L.mm_last_error.restype = ctypes.c_char_p
     L.mm_version.argtypes = []; L.mm_version.restype = ctypes.c_char_p
     L.mm_set_allocator.argtypes = [vp, vp, vp]; L.mm_set_allocator.restype = ctypes.c_int
+    L.mm_validate_sset.argtypes = [P(mm_sset), vp]; L.mm_validate_sset.restype = ctypes.c_int
     L.mm_sweep_workspace.argtypes = [i32, ctypes.c_int, P(mm_approx), P(ctypes.c_size_t)]
     L.mm_sweep_workspace.restype = ctypes.c_int
     L.mm_sweep.argtypes = [P(mm_sset), ctypes.c_int, f32, f32, P(mm_approx), vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -410,3 +412,9 @@ def full_stress(g: DeviceGraph, x):
     gs = g.c_struct()
     _check(L.mm_full_stress(ctypes.byref(gs), _dim_of(x), _ptr(x), out, _stream_ptr(x.device)), "mm_full_stress")
     return float(out[0]), float(out[1]), float(out[2]), int(out[3])
+
+
+def validate_sset(S: DeviceSSet):
+    """Device-side validation of an S set (raises MMError(MM_ERR_INVALID_INPUT))."""
+    s = S.c_struct()
+    _check(load().mm_validate_sset(ctypes.byref(s), _stream_ptr(S.row_ptr.device)), "mm_validate_sset")

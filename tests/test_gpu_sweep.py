@@ -202,3 +202,32 @@ def test_nonfinite_flag(mm):
     x[5, 0] = np.nan
     _, st = _gpu_sweep(mm, w.S, x, w.alpha, w.q, stats=True)
     assert st["flags"] & 1
+
+
+def test_validate_sset(mm):
+    """mm_validate_sset flags each documented input error (MM_ERR_INVALID_INPUT)."""
+    import torch
+
+    w = workload("cfg1")
+    mm.validate_sset(mm.sset_to_device(w.S))  # valid
+    cases = []
+    S = mm.sset_to_device(w.S)
+    S.d[3] = 0.0
+    cases.append((S, "d <= 0"))
+    S = mm.sset_to_device(w.S)
+    S.w[5] = float("nan")
+    cases.append((S, "w < 0"))
+    S = mm.sset_to_device(w.S)
+    S.col[7] = w.n + 3
+    cases.append((S, "out of range"))
+    S = mm.sset_to_device(w.S)
+    S.col[int(w.S.row_ptr[2])] = 2
+    cases.append((S, "self entry"))
+    S = mm.sset_to_device(w.S)
+    S.w[int(w.S.row_ptr[9]):int(w.S.row_ptr[10])] = 0.0
+    cases.append((S, "rho_i <= 0"))
+    for S, what in cases:
+        with pytest.raises(mm.MMError) as ei:
+            mm.validate_sset(S)
+        assert ei.value.status == -2 and what in str(ei.value), (what, str(ei.value))
+    torch.cuda.synchronize()

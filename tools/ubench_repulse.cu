@@ -11,9 +11,9 @@ LaunchScope::~LaunchScope() {}
 }
 using namespace mm;
 
-template <int T, int BM, int MINB>
+template <int T, int BM, int MINB, int UNR = 4>
 void run(int n, const float* x, float* part, int sms) {
-    auto kern = k_repulse<2, false, false, T, BM, MINB>;
+    auto kern = k_repulse<2, false, false, T, BM, MINB, UNR>;
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
     Sched s;
@@ -37,8 +37,8 @@ void run(int n, const float* x, float* part, int sms) {
     cudaEventElapsedTime(&ms, a, b);
     ms /= reps;
     const double pairs = (double)n * n;
-    printf("T=%d BMASK=%d MINB=%d regs=%d occ=%d G=%d  %.4f ms  %.4e pairs/s  (%.1f%% of 16 MUFU/clk/SM @1965)\n", T, BM,
-           MINB, fa.numRegs, occ, s.G, ms, pairs / (ms * 1e-3), 100.0 * pairs / (ms * 1e-3) / (148 * 16 * 1.965e9));
+    printf("T=%d BMASK=%d MINB=%d UNR=%d regs=%d occ=%d G=%d  %.4f ms  %.4e pairs/s  (%.1f%% of 16 MUFU/clk/SM @1965)\n", T, BM,
+           MINB, UNR, fa.numRegs, occ, s.G, ms, pairs / (ms * 1e-3), 100.0 * pairs / (ms * 1e-3) / (148 * 16 * 1.965e9));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) printf("  error %s\n", cudaGetErrorString(e));
 }
@@ -86,24 +86,19 @@ int main(int argc, char** argv) {
     cudaMalloc(&x, hx.size() * 4);
     cudaMalloc(&part, (size_t)n * 2 * 4 * 64);
     cudaMemcpy(x, hx.data(), hx.size() * 4, cudaMemcpyHostToDevice);
-    run<4, 0, 1>(n, x, part, sms);
-    run<4, 1, 1>(n, x, part, sms);
-    run<4, 3, 1>(n, x, part, sms);
-    run<4, 0, 6>(n, x, part, sms);
-    run<4, 1, 6>(n, x, part, sms);
-    run<2, 0, 1>(n, x, part, sms);
-    run<2, 1, 1>(n, x, part, sms);
-    run<6, 0, 1>(n, x, part, sms);
-    run<6, 1, 1>(n, x, part, sms);
-    run<6, 3, 1>(n, x, part, sms);
-    run<8, 0, 1>(n, x, part, sms);
-    run<8, 1, 1>(n, x, part, sms);
-    run<8, 5, 1>(n, x, part, sms);
-    run<8, 3, 1>(n, x, part, sms);
-    run<8, 7, 1>(n, x, part, sms);
-    run<8, 1, 3>(n, x, part, sms);
-    run<12, 1, 1>(n, x, part, sms);
-    run<12, 9, 1>(n, x, part, sms);
+    run<4, 1, 1, 1>(n, x, part, sms);
+    run<4, 1, 1, 2>(n, x, part, sms);
+    run<4, 1, 1, 4>(n, x, part, sms);
+    run<4, 1, 1, 8>(n, x, part, sms);
+    run<4, 1, 3, 2>(n, x, part, sms);
+    run<4, 1, 3, 1>(n, x, part, sms);
+    run<4, 1, 4, 1>(n, x, part, sms);
+    run<2, 1, 1, 8>(n, x, part, sms);
+    run<2, 1, 4, 4>(n, x, part, sms);
+    run<6, 1, 1, 2>(n, x, part, sms);
+    run<6, 5, 1, 2>(n, x, part, sms);
+    run<8, 1, 1, 2>(n, x, part, sms);
+    run<8, 5, 2, 1>(n, x, part, sms);
     // coarse: n = 262,144 targets in [0,512)^2, k = 77,649 reps (cfg3 finest level shape)
     {
         const int nt = 262144, k = 77649;
