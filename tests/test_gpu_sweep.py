@@ -231,3 +231,44 @@ def test_validate_sset(mm):
             mm.validate_sset(S)
         assert ei.value.status == -2 and what in str(ei.value), (what, str(ei.value))
     torch.cuda.synchronize()
+
+
+def test_two_path_orbit_gpu(mm):
+    """P1 on the GPU: K2 maps the separation s to (2d - |s|) s_hat, midpoint fixed."""
+    g = H.path(2)
+    S = H.sset_with(g, [1.0, 1.0])
+    x = np.array([[0.0, 0.0], [1.5, 0.0]], dtype=np.float32)
+    y = _gpu_sweep(mm, S, x, 0.3, 0.0)
+    np.testing.assert_allclose(y, [[0.5, 0.0], [1.0, 0.0]], atol=1e-6)
+    z = _gpu_sweep(mm, S, y.astype(np.float32), 0.3, 0.0)
+    np.testing.assert_allclose(z, x, atol=1e-6)
+
+
+def test_exact_sweep_3d_q0(mm):
+    w = workload("cfg5_grid12")
+    x = configs.random_state(w.n, 3, seed=8, scale=12.0)
+    got = _gpu_sweep(mm, w.S, x, w.alpha, 0.0)
+    want = oracle.sweep_exact(w.S, x.astype(np.float64), w.alpha, 0.0)
+    assert_sweep_parity(got, want, "grid12^3 q=0")
+
+
+def test_empty_and_degenerate_inputs_rejected(mm):
+    import ctypes
+
+    from paper_1506_04383_b200 import mulment
+
+    L = mm.load()
+    s = mulment.mm_sset(0, 0, 0x1000, None, None, None)
+    rc = L.mm_sweep(ctypes.byref(s), 2, 0.1, 0.0, None, 0x5000, 0x6000, None, None, 0, None)
+    assert rc == mulment.MM_ERR_INVALID_ARGUMENT
+    out = (ctypes.c_double * 4)()
+    g = mulment.mm_graph(0, 0, 0x1000, None, None)
+    assert L.mm_full_stress(ctypes.byref(g), 2, 0x5000, out, None) == mulment.MM_ERR_INVALID_ARGUMENT
+    # approximate sweep with k out of range
+    w = workload("cfg1")
+    import torch
+    Sd = mm.sset_to_device(w.S)
+    xd = mm.coords_to_device(w.x0)
+    par = torch.zeros(w.n, dtype=torch.int32, device="cuda")
+    with pytest.raises(mm.MMError):
+        mm.sweep(Sd, xd, 0.1, 0.0, parent=par, ancestor=par, k=w.n + 1)
