@@ -113,3 +113,20 @@ def test_layout_in_place(mm):
     x2, rep = mm.layout(None, S, 2, w.alpha, w.q, 0, [3], w.seed, x_init=xd, out=xd)
     xo, eo, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [3], w.seed, x_init=w.x0.astype(np.float64))
     assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL
+
+
+def test_layout_bitwise_deterministic(mm):
+    """Two multilevel runs (cached CUDA graphs, persistent schedule, fixed-order
+    reductions) give bitwise identical layouts and energies."""
+    w = workload("cfg3_mesh64")
+    g, S = mm.graph_to_device(w.graph), mm.sset_to_device(w.S)
+    xa, ra = mm.layout(g, S, 2, w.alpha, w.q, 2, [5], w.seed, n_stop=200)
+    a = xa.cpu().numpy().copy()
+    xb, rb = mm.layout(g, S, 2, w.alpha, w.q, 2, [5], w.seed, n_stop=200)
+    assert np.array_equal(a, xb.cpu().numpy()) and ra["energy"] == rb["energy"]
+    xs1, r1 = mm.layout_schedule(g, S, 2, 0.0, 2, mm.paper_schedule(max_final_iters=5), w.seed, n_stop=200,
+                                 sclap=True, disc=True)
+    s1 = xs1.cpu().numpy().copy()
+    xs2, r2 = mm.layout_schedule(g, S, 2, 0.0, 2, mm.paper_schedule(max_final_iters=5), w.seed, n_stop=200,
+                                 sclap=True, disc=True)
+    assert np.array_equal(s1, xs2.cpu().numpy()) and r1["sweeps_level"] == r2["sweeps_level"]
