@@ -341,6 +341,13 @@ def run_gpu(args):
     if w.q != 0.0:
         flop_pair += 3
     achieved_tflops = flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
+    # kernel (b) variant: the symmetric kernel evaluates every unordered pair
+    # once, so it EXECUTES (flop_pair + 2 dim)/2 flop per ordered
+    # pair (the j-side accumulation costs 2 dim) while the algorithmic count
+    # stays flop_pair per ordered pair interaction of Eq.(2)
+    sym = hh == 0 and mm.exact_kernel_variant(n, w.dim) == 1
+    exec_flop_pair = (flop_pair + 2 * w.dim) / 2.0 if sym else float(flop_pair)
+    executed_tflops = exec_flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
     step_share = {k: v["total_ms"] / max(dev_ms, 1e-9) for k, v in prof.items()}
     gpu_ms = sum(v["total_ms"] for v in prof.values())
     gpu_share = {k: v["total_ms"] / max(gpu_ms, 1e-9) for k, v in prof.items()}
@@ -377,7 +384,10 @@ def run_gpu(args):
                      "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (DESIGN.md §5)",
                      "flop_per_pair": flop_pair, "pairs_per_launch": pairs_launch,
                      "avg_launch_ms": k_ms,
-                     "mufu_ceiling_frac": MUFU_PER_CLK_SM * FLOP_PER_PAIR / (2.0 * FP32_LANES),
+                     "kernel_variant": "symmetric" if sym else "one-sided",
+                     "executed_flop_per_pair": exec_flop_pair,
+                     "executed_tflops": executed_tflops, "executed_frac": executed_tflops / FP32_PEAK_TFLOPS,
+                     "mufu_ceiling_frac": None if sym else MUFU_PER_CLK_SM * FLOP_PER_PAIR / (2.0 * FP32_LANES),
                      "pairs_per_s_kernel": pairs_launch / (k_ms / 1e3)},
         "levels": rep["n_level"], "k_levels": rep["k_level"],
         "kernel_share_of_step": step_share,

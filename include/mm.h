@@ -265,6 +265,12 @@ MM_API mm_status mm_full_stress(const mm_graph* g, int dim, const float* x, doub
 /* ------------------------------------------------------------------ instrumentation */
 /* Total kernels launched by this library since load (host counter). */
 MM_API int64_t mm_launch_count(void);
+/* Which kernel (b) an exact sweep of n vertices in `dim` dimensions uses:
+ * 0 = one-sided tiled kernel (every ordered pair evaluated), 1 = symmetric
+ * kernel (every unordered pair evaluated once and applied to both vertices,
+ * DESIGN.md §5).  Host-only query (no GPU work; needs a current device for the
+ * SM count); environment MM_SYM=0 forces 0, MM_SYM=2 forces 1. */
+MM_API int mm_exact_kernel_variant(int32_t n, int dim);
 /* When enabled, every kernel launch is bracketed by CUDA events on its
  * stream; mm_profile_read syncs those events and returns, per kernel name,
  * the launch count and summed device milliseconds. */

@@ -208,6 +208,7 @@ mm_status check_x(const float* x, int dim, const char* what, const char* who) {
 // Buffers for one sweep (all device); sized by plan_sweep_bytes.
 struct SweepBufs {
     float* part = nullptr;
+    float* jpart = nullptr;  // symmetric exact mode: j-side sums [TB-1][n]
     double* stat_partial = nullptr;
     int32_t* flags = nullptr;
     float4* rep_hi = nullptr;
@@ -227,12 +228,38 @@ size_t cub_tmp_bytes(int32_t n) {
     return std::max(sort_temp_bytes_i32(n), scan_temp_bytes(n + 2)) + 256;
 }
 
-size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) {
-    const int32_t n_src = approx ? k : n;
+// Exact sweeps use the symmetric kernel (each unordered pair once)
+// unless MM_SYM=0, its j-side buffer would exceed 2 GiB, or the triangular
+// schedule has too few units per CTA; MM_SYM=2 forces it (tests).
+bool use_sym(int32_t n, int dim) {
+    static int env = -1;
+    if (env < 0) {
+        const char* v = getenv("MM_SYM");
+        env = (v && v[0] == '0') ? 0 : (v && v[0] == '2') ? 2 : 1;  // 2: force (tests)
+    }
+    if (!env) return false;
+    const int64_t tb = (n + 1023) / 1024;
+    if ((tb - 1) * (int64_t)n * stride_of(dim) * 4 > (int64_t(1) << 31)) return false;
+    // the triangular schedule has only TB(TB+1)/2 block-pair units: below ~4 per
+    // CTA its load imbalance costs more than the halved pair count saves
+    const SymPlan sp = plan_repulse_sym(n, dim);
+    return env == 2 || sp.ts.U >= 4 * (int64_t)sp.ts.G;
+}
+
+int part_slots(int32_t n, int dim, int32_t n_src, bool approx) {
     RepulsePlan p = plan_repulse(n, n_src, dim, approx, true);
     RepulsePlan p2 = plan_repulse(n, n_src, dim, approx, false);
-    const int slots = std::max(p.slots, p2.slots);
+    int slots = std::max(p.slots, p2.slots);
+    if (!approx && use_sym(n, dim)) slots = std::max(slots, plan_repulse_sym(n, dim).slots);
+    return slots;
+}
+
+size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) {
+    const int32_t n_src = approx ? k : n;
+    const int slots = part_slots(n, dim, n_src, approx);
     size_t b = al((size_t)slots * n * stride_of(dim) * sizeof(float));
+    if (!approx && use_sym(n, dim))
+        b += al((size_t)sym_jpart_rows(plan_repulse_sym(n, dim)) * n * stride_of(dim) * sizeof(float));
     (void)mean_row;
     b += al((size_t)gather_blocks(n, 1e9) * 3 * sizeof(double));  // bound: G = 32
     b += al(sizeof(int32_t) * 4);
@@ -247,9 +274,9 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
 
 bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double mean_row, SweepBufs& sb) {
     const int32_t n_src = approx ? k : n;
-    RepulsePlan p = plan_repulse(n, n_src, dim, approx, true);
-    RepulsePlan p2 = plan_repulse(n, n_src, dim, approx, false);
-    sb.part = cv.take<float>((size_t)std::max(p.slots, p2.slots) * n * stride_of(dim));
+    sb.part = cv.take<float>((size_t)part_slots(n, dim, n_src, approx) * n * stride_of(dim));
+    if (!approx && use_sym(n, dim))
+        sb.jpart = cv.take<float>((size_t)sym_jpart_rows(plan_repulse_sym(n, dim)) * n * stride_of(dim));
     (void)mean_row;
     sb.stat_partial = cv.take<double>((size_t)gather_blocks(n, 1e9) * 3);
     sb.flags = cv.take<int32_t>(4);
@@ -286,11 +313,15 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     const bool qpow = q != 0.0f;
     cudaError_t e;
     RepulsePlan p;
+    SymPlan sp;
     if (ap) {
         e = launch_centroid(dim, ap->k, sb.mptr, sb.mem, x_in, sb.rep_hi, sb.rep_lo, st);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
         e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, ap->ancestor, p, sb.part, st);
+    } else if (sb.jpart) {
+        sp = plan_repulse_sym(n, dim);
+        e = launch_repulse_sym(dim, qpow, q, n, x_in, sp, sb.part, sb.jpart, st);
     } else {
         p = plan_repulse(n, n, dim, false, qpow);
         e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, nullptr, p, sb.part, st);
@@ -308,6 +339,12 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     ga.part = sb.part;
     ga.sch = p.sch;
     ga.tpb = repulse_targets_per_block(dim);
+    ga.jpart = nullptr;
+    if (!ap && sb.jpart) {
+        ga.jpart = sb.jpart;
+        ga.tri = sp.ts;
+        ga.tpb = 1024;
+    }
     ga.parent = ap ? ap->parent : nullptr;
     ga.child_ptr = ap ? sb.cptr : nullptr;
     ga.child = ap ? sb.child : nullptr;
@@ -471,6 +508,11 @@ mm_status mm_energy(const mm_sset* S, int dim, double alpha, double q, const flo
 }
 
 int64_t mm_launch_count(void) { return g_launches.load(); }
+
+int mm_exact_kernel_variant(int32_t n, int dim) {
+    if (n < 1 || (dim != 2 && dim != 3)) return 0;
+    return use_sym(n, dim) ? 1 : 0;
+}
 
 mm_status mm_profile_enable(int on) {
     g_prof_on.store(on ? 1 : 0);

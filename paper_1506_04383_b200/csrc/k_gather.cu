@@ -80,13 +80,25 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 // first so that their latency overlaps the S-row loads
                 const int stride = DIM == 2 ? 2 : 4;
                 const int64_t tb = i / a.tpb;
-                const int32_t nslot = sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
-                                      sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
+                const int32_t nslot =
+                    a.jpart ? sched_first_cta_tri(tri_prefix((int32_t)tb + 1, a.tri) - 1, a.tri) -
+                                  sched_first_cta_tri(tri_prefix((int32_t)tb, a.tri), a.tri) + 1
+                            : sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
+                                  sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
                 for (int p = 0; p < nslot; ++p) {
                     const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
                     R.x += v.x;
                     R.y += v.y;
                     R.z += v.z;
+                }
+                // symmetric mode: j-side sums of the block pairs (I, tb), I < tb
+                if (a.jpart) {
+                    for (int64_t I = 0; I < tb; ++I) {
+                        const float4 v = load_x<DIM>(a.jpart + I * a.n * stride, i);
+                        R.x += v.x;
+                        R.y += v.y;
+                        R.z += v.z;
+                    }
                 }
             }
             const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];

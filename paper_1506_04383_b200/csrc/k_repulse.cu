@@ -181,6 +181,232 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
     }
 }
 
+// ---------------------------------------------------------------------------
+// Symmetric exact repulsion (kernel (b), default for exact sweeps): every
+// unordered pair is evaluated once and applied to both vertices, using the
+// exact FP32 antisymmetry of the pair term (x_j - x_i = -(x_i - x_j) exactly,
+// same r^2, same reciprocal).  Blocks of kSymTPB vertices; the work units are
+// the block pairs (I, J >= I) of a triangular persistent schedule.
+//  * I == J: every ordered pair inside the block on the target side only
+//    (the plain loop; the self pair contributes exactly 0).
+//  * I <  J: warp w owns 64*SG targets of I (2*SG per lane, in registers); the
+//    sources of J are taken 32 at a time, one per lane, and rotated through
+//    the lanes in 32 shuffle steps together with their own accumulators, so
+//    each lane meets every source of the chunk; after the 32 steps every
+//    source's j-side sum (over the warp's targets) is back in its home lane.
+//    The warps' j-side sums are added in warp order in shared memory and
+//    written to jpart[I][j]; target sums go to ipart[slot][i] as in k_repulse.
+// Kernel (a) adds, for vertex i of block B, its i-side slots and jpart[I][i]
+// for I < B, in that fixed order: the result is bitwise deterministic.
+constexpr int kSymTPB = 1024;  // vertices per block (targets = sources)
+
+#ifndef MM_SYM_SRC
+#define MM_SYM_SRC 256
+#endif
+constexpr int kSymSrc = MM_SYM_SRC;  // sources per shared-memory sub-tile
+template <int DIM>
+constexpr int sym_smem_bytes(int warps) {
+    return kSymSrc * 16 + warps * kSymSrc * (DIM == 2 ? 2 : 3) * 4;
+}
+
+#ifndef MM_SYM_UNR
+#define MM_SYM_UNR 8
+#endif
+constexpr int kSymUnroll = MM_SYM_UNR;
+// one 32-step rotation over a chunk of 32 sources; MASK: the chunk is the
+// partial tail of the last block (lanes past the end carry weight 0)
+template <int DIM, bool QPOW, int SG, bool MASK>
+__device__ __forceinline__ void sym_chunk(const f2x (&X)[SG], const f2x (&Y)[SG], const f2x (&Z)[SG], f2x (&AX)[SG],
+                                          f2x (&AY)[SG], f2x (&AZ)[SG], float4 sv, float sw, float cexp, int lane,
+                                          float& bx_out, float& by_out, float& bz_out) {
+    const f2x eps2 = pk(kEps2, kEps2);
+    float sx = sv.x, sy = sv.y, sz = sv.z;
+    float bx = 0.f, by = 0.f, bz = 0.f;
+    const int nxt = (lane + 1) & 31;
+#pragma unroll kSymUnroll
+    for (int k = 0; k < 32; ++k) {
+#pragma unroll
+        for (int gg = 0; gg < SG; ++gg) {
+            const f2x dx = sub_bc(X[gg], sx), dy = sub_bc(Y[gg], sy);
+            f2x r2 = fma2(dx, dx, eps2);
+            r2 = fma2(dy, dy, r2);
+            f2x dz = 0ull;
+            if constexpr (DIM == 3) {
+                dz = sub_bc(Z[gg], sz);
+                r2 = fma2(dz, dz, r2);
+            }
+            f2x inv = (gg & 1) == 0 ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+            if constexpr (MASK) inv = mul2(inv, pk(sw, sw));
+            AX[gg] = fma2(dx, inv, AX[gg]);
+            AY[gg] = fma2(dy, inv, AY[gg]);
+            if constexpr (DIM == 3) AZ[gg] = fma2(dz, inv, AZ[gg]);
+            // j side: sum_t (x_j - x_t) inv_t = -sum_t dx_t inv_t
+            float i0, i1, a0, a1;
+            upk(inv, i0, i1);
+            upk(dx, a0, a1);
+            bx = fmaf(-a0, i0, bx);
+            bx = fmaf(-a1, i1, bx);
+            upk(dy, a0, a1);
+            by = fmaf(-a0, i0, by);
+            by = fmaf(-a1, i1, by);
+            if constexpr (DIM == 3) {
+                upk(dz, a0, a1);
+                bz = fmaf(-a0, i0, bz);
+                bz = fmaf(-a1, i1, bz);
+            }
+        }
+        // rotate the source and its accumulator: lane l takes lane l+1's
+        sx = __shfl_sync(0xffffffffu, sx, nxt);
+        sy = __shfl_sync(0xffffffffu, sy, nxt);
+        bx = __shfl_sync(0xffffffffu, bx, nxt);
+        by = __shfl_sync(0xffffffffu, by, nxt);
+        if constexpr (DIM == 3) {
+            sz = __shfl_sync(0xffffffffu, sz, nxt);
+            bz = __shfl_sync(0xffffffffu, bz, nxt);
+        }
+        if constexpr (MASK) sw = __shfl_sync(0xffffffffu, sw, nxt);
+    }
+    bx_out = bx;
+    by_out = by;
+    bz_out = bz;
+}
+
+#ifndef MM_SYM_MINB
+#define MM_SYM_MINB 3
+#endif
+template <int DIM, bool QPOW, int SG, int WARPS, int SRC>
+__global__ void __launch_bounds__(WARPS * 32, MM_SYM_MINB) k_repulse_sym(int32_t n, const float* __restrict__ x, float cexp,
+                                                            TriSched ts, float* __restrict__ ipart,
+                                                            float* __restrict__ jpart) {
+    static_assert(WARPS * 64 * SG == kSymTPB, "a block is one target set");
+    constexpr int NT = WARPS * 32;
+    constexpr int stride = DIM == 2 ? 2 : 4;
+    constexpr int DC = DIM == 2 ? 2 : 3;
+    extern __shared__ float4 sym_smem[];
+    float4* src = sym_smem;                                 // [SRC]
+    float* jacc = reinterpret_cast<float*>(sym_smem + SRC);  // [WARPS][SRC][DC]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int32_t g = blockIdx.x;
+    const int64_t u0 = (int64_t)g * ts.U / ts.G, u1 = (int64_t)(g + 1) * ts.U / ts.G;
+    const f2x eps2 = pk(kEps2, kEps2);
+    for (int64_t u = u0; u < u1;) {
+        int32_t lo = 0, hi = ts.TB - 1;
+        while (lo < hi) {
+            const int32_t mid = (lo + hi + 1) >> 1;
+            if (tri_prefix(mid, ts) <= u) lo = mid; else hi = mid - 1;
+        }
+        const int32_t I = lo;
+        const int64_t pre = tri_prefix(I, ts);
+        const int64_t seg_end = min(u1, tri_prefix(I + 1, ts));
+        const int64_t ibase = (int64_t)I * kSymTPB;
+        // this warp's targets: ibase + warp*64*SG + 32*k + lane, k = 0..2SG-1
+        f2x X[SG], Y[SG], Z[SG], AX[SG], AY[SG], AZ[SG];
+#pragma unroll
+        for (int gg = 0; gg < SG; ++gg) {
+            const int64_t ia = ibase + warp * 64 * SG + (2 * gg) * 32 + lane, ib = ia + 32;
+            const int64_t ca = ia < n ? ia : n - 1, cb = ib < n ? ib : n - 1;
+            const float* pa = x + ca * stride;
+            const float* pb = x + cb * stride;
+            X[gg] = pk(__ldg(pa), __ldg(pb));
+            Y[gg] = pk(__ldg(pa + 1), __ldg(pb + 1));
+            Z[gg] = (DIM == 3) ? pk(__ldg(pa + 2), __ldg(pb + 2)) : 0ull;
+            AX[gg] = AY[gg] = AZ[gg] = 0ull;
+        }
+        for (; u < seg_end; ++u) {
+            const int32_t J = I + (int32_t)(u - pre);
+            const int64_t jblk = (int64_t)J * kSymTPB;
+            const int jtot = (int)min((int64_t)kSymTPB, (int64_t)n - jblk);
+            // sources of J in sub-tiles of SRC (small shared footprint -> more resident warps)
+            for (int s0 = 0; s0 < jtot; s0 += SRC) {
+                const int64_t jbase = jblk + s0;
+                const int jcnt = min(SRC, jtot - s0);
+                __syncthreads();
+                for (int t = tid; t < SRC; t += NT)
+                    src[t] = (t < jcnt) ? load_x<DIM>(x, jbase + t) : make_float4(0.f, 0.f, 0.f, 0.f);
+                __syncthreads();
+                if (J == I) {
+                    // diagonal block: all ordered pairs on the target side (self -> 0)
+#pragma unroll 4
+                    for (int jj = 0; jj < jcnt; ++jj) {
+                        const float4 sv = src[jj];
+#pragma unroll
+                        for (int gg = 0; gg < SG; ++gg) {
+                            const f2x dx = sub_bc(X[gg], sv.x), dy = sub_bc(Y[gg], sv.y);
+                            f2x r2 = fma2(dx, dx, eps2);
+                            r2 = fma2(dy, dy, r2);
+                            f2x dz = 0ull;
+                            if constexpr (DIM == 3) {
+                                dz = sub_bc(Z[gg], sv.z);
+                                r2 = fma2(dz, dz, r2);
+                            }
+                            const f2x inv =
+                                (gg & 1) == 0 ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+                            AX[gg] = fma2(dx, inv, AX[gg]);
+                            AY[gg] = fma2(dy, inv, AY[gg]);
+                            if constexpr (DIM == 3) AZ[gg] = fma2(dz, inv, AZ[gg]);
+                        }
+                    }
+                    continue;
+                }
+                // off-diagonal (I < J, so block I is full): rotation over 32-source chunks
+                const int nfull = jcnt >> 5;
+                for (int c = 0; c < nfull; ++c) {
+                    float bx, by, bz;
+                    sym_chunk<DIM, QPOW, SG, false>(X, Y, Z, AX, AY, AZ, src[c * 32 + lane], 1.f, cexp, lane, bx, by,
+                                                    bz);
+                    float* jw = jacc + ((int64_t)warp * SRC + c * 32 + lane) * DC;
+                    jw[0] = bx;
+                    jw[1] = by;
+                    if constexpr (DIM == 3) jw[2] = bz;
+                }
+                if (jcnt & 31) {
+                    const int c = nfull;
+                    float bx, by, bz;
+                    sym_chunk<DIM, QPOW, SG, true>(X, Y, Z, AX, AY, AZ, src[c * 32 + lane],
+                                                   (c * 32 + lane) < jcnt ? 1.f : 0.f, cexp, lane, bx, by, bz);
+                    float* jw = jacc + ((int64_t)warp * SRC + c * 32 + lane) * DC;
+                    jw[0] = bx;
+                    jw[1] = by;
+                    if constexpr (DIM == 3) jw[2] = bz;
+                }
+                __syncthreads();
+                // j-side partial of block pair (I, J): warps added in warp order
+                float* jo = jpart + (int64_t)I * n * stride;
+                for (int t = tid; t < jcnt; t += NT) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int w = 0; w < WARPS; ++w) {
+                        const float* jr = jacc + ((int64_t)w * SRC + t) * DC;
+                        v.x += jr[0];
+                        v.y += jr[1];
+                        if constexpr (DIM == 3) v.z += jr[2];
+                    }
+                    store_x<DIM>(jo, jbase + t, v);
+                }
+            }
+        }
+        // target side of row I handled by this CTA -> slot g - first CTA of the row
+        const int32_t slot = g - sched_first_cta_tri(pre, ts);
+        float* out = ipart + (int64_t)slot * n * stride;
+#pragma unroll
+        for (int gg = 0; gg < SG; ++gg) {
+            const int64_t ia = ibase + warp * 64 * SG + (2 * gg) * 32 + lane, ib = ia + 32;
+            float ax0, ax1, ay0, ay1, az0 = 0.f, az1 = 0.f;
+            upk(AX[gg], ax0, ax1);
+            upk(AY[gg], ay0, ay1);
+            if constexpr (DIM == 3) upk(AZ[gg], az0, az1);
+            if (ia < n) store_x<DIM>(out, ia, make_float4(ax0, ay0, az0, 0.f));
+            if (ib < n) store_x<DIM>(out, ib, make_float4(ax1, ay1, az1, 0.f));
+        }
+    }
+}
+
+#ifndef MM_SYM_SG
+#define MM_SYM_SG 2
+#endif
+constexpr int kSymSG = MM_SYM_SG;
+constexpr int kSymWarps = kSymTPB / (64 * kSymSG);
+
 // All-pairs entropy for mm_energy over UNORDERED pairs i < j (the ordered sum
 // of Eq.(1) in the S form is  1/2 sum_{i != j} phi - 1/2 sum_i sum_{S_i} phi
 // = sum_{i<j} phi - 1/2 sum_S phi, valid for asymmetric S too):
@@ -415,6 +641,70 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
 }
 
 int repulse_targets_per_block(int dim) { return kBlock * targets_per_thread(dim); }
+
+namespace {
+template <int DIM, bool QPOW>
+cudaError_t sym_launch(int32_t n, const float* x, float cexp, const TriSched& ts, float* ipart, float* jpart,
+                       cudaStream_t st) {
+    constexpr int smem = sym_smem_bytes<DIM>(kSymWarps);
+    auto* fn = k_repulse_sym<DIM, QPOW, kSymSG, kSymWarps, kSymSrc>;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    fn<<<ts.G, kSymWarps * 32, smem, st>>>(n, x, cexp, ts, ipart, jpart);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+SymPlan plan_repulse_sym(int32_t n, int dim) {
+    SymPlan p;
+    TriSched& t = p.ts;
+    t.TB = (int32_t)((n + kSymTPB - 1) / kSymTPB);
+    t.Ub = t.TB;
+    t.c = 1;
+    t.U = tri_prefix(t.TB, t);
+    static int occ[2] = {0, 0};
+    int& o = occ[dim == 3];
+    if (!o) {
+        int v = 0;
+        if (dim == 2) {
+            cudaFuncSetAttribute(k_repulse_sym<2, false, kSymSG, kSymWarps, kSymSrc>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem_bytes<2>(kSymWarps));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_repulse_sym<2, false, kSymSG, kSymWarps, kSymSrc>,
+                                                          kSymWarps * 32, sym_smem_bytes<2>(kSymWarps));
+        } else {
+            cudaFuncSetAttribute(k_repulse_sym<3, false, kSymSG, kSymWarps, kSymSrc>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem_bytes<3>(kSymWarps));
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_repulse_sym<3, false, kSymSG, kSymWarps, kSymSrc>,
+                                                          kSymWarps * 32, sym_smem_bytes<3>(kSymWarps));
+        }
+        o = std::max(v, 1);
+    }
+    t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * o, t.U));
+    int32_t ms = 1;
+    for (int32_t I = 0; I < t.TB; ++I) {
+        const int32_t a = sched_first_cta_tri(tri_prefix(I, t), t);
+        const int32_t b = sched_first_cta_tri(tri_prefix(I + 1, t) - 1, t);
+        ms = std::max(ms, b - a + 1);
+    }
+    p.slots = ms;
+    return p;
+}
+
+int64_t sym_jpart_rows(const SymPlan& p) { return std::max<int64_t>(p.ts.TB - 1, 1); }
+
+cudaError_t launch_repulse_sym(int dim, bool qpow, float q, int32_t n, const float* x, const SymPlan& p,
+                               float* ipart, float* jpart, cudaStream_t st) {
+    const float cexp = -(q + 2.0f) * 0.5f;
+    LaunchScope ls("repulse_exact", st);
+    if (dim == 2) return qpow ? sym_launch<2, true>(n, x, cexp, p.ts, ipart, jpart, st)
+                              : sym_launch<2, false>(n, x, cexp, p.ts, ipart, jpart, st);
+    return qpow ? sym_launch<3, true>(n, x, cexp, p.ts, ipart, jpart, st)
+                : sym_launch<3, false>(n, x, cexp, p.ts, ipart, jpart, st);
+}
 
 EntropyPlan plan_entropy(int32_t n) {
     EntropyPlan p;

@@ -34,6 +34,18 @@ struct TriSched {
 __host__ __device__ __forceinline__ int64_t tri_prefix(int32_t tb, const TriSched& s) {
     return (int64_t)tb * s.Ub - (int64_t)s.c * tb * (tb - 1) / 2;
 }
+// first CTA whose range of a triangular schedule contains unit a (same rule as sched_first_cta)
+__host__ __device__ __forceinline__ int32_t sched_first_cta_tri(int64_t a, const TriSched& s) {
+    return (int32_t)(((a + 1) * (int64_t)s.G - 1) / s.U);
+}
+struct SymPlan {
+    TriSched ts;   // blocks of 1024 vertices; units = block pairs (I, J >= I)
+    int slots = 1; // max i-side partial slots per vertex
+};
+SymPlan plan_repulse_sym(int32_t n, int dim);
+int64_t sym_jpart_rows(const SymPlan& p);  // rows I of jpart[I][n] (blocks 0..TB-2)
+cudaError_t launch_repulse_sym(int dim, bool qpow, float q, int32_t n, const float* x, const SymPlan& p,
+                               float* ipart, float* jpart, cudaStream_t st);
 struct EntropyPlan {
     TriSched ts;
     int nblocks = 1;   // CTAs = FP64 partials
@@ -61,6 +73,10 @@ struct GatherArgs {
     const float* part;   // [slots][n] stride 2 (dim 2) or 4 (dim 3)
     Sched sch;           // schedule that produced `part` (slot count per target block)
     int tpb;             // targets per block of that schedule
+    // symmetric exact mode (k_repulse_sym): i-side slots follow the triangular
+    // schedule `tri`; jpart[I][i] for I < block(i) holds the j-side sums
+    const float* jpart = nullptr;  // nullable: rectangular schedule
+    TriSched tri;
     // Eq.(3) sibling term (nullable: exact mode)
     const int32_t* parent;
     const int32_t* child_ptr;

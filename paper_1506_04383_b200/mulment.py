@@ -25,7 +25,7 @@ EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator"
            "mm_sweep_workspace",
            "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_build_hierarchy_sclap", "mm_hierarchy_num_levels", "mm_hierarchy_level",
            "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_full_stress",
-           "mm_launch_count",
+           "mm_launch_count", "mm_exact_kernel_variant",
            "mm_profile_enable",
            "mm_profile_reset", "mm_profile_read"]
 
@@ -133,6 +133,7 @@ def load() -> ctypes.CDLL:
     L.mm_full_stress.argtypes = [P(mm_graph), ctypes.c_int, vp, P(f64), vp]
     L.mm_full_stress.restype = ctypes.c_int
     L.mm_launch_count.argtypes = []; L.mm_launch_count.restype = i64
+    L.mm_exact_kernel_variant.argtypes = [i32, ctypes.c_int]; L.mm_exact_kernel_variant.restype = ctypes.c_int
     L.mm_profile_enable.argtypes = [ctypes.c_int]; L.mm_profile_enable.restype = ctypes.c_int
     L.mm_profile_reset.argtypes = []; L.mm_profile_reset.restype = ctypes.c_int
     L.mm_profile_read.argtypes = [P(mm_kernel_profile), i32, P(i32)]; L.mm_profile_read.restype = ctypes.c_int
@@ -385,6 +386,11 @@ def layout_schedule(g: Optional[DeviceGraph], S: DeviceSSet, dim: int, q: float,
 
 def launch_count() -> int:
     return int(load().mm_launch_count())
+
+
+def exact_kernel_variant(n: int, dim: int) -> int:
+    """0: one-sided kernel (b); 1: symmetric kernel (b)."""
+    return int(load().mm_exact_kernel_variant(int(n), int(dim)))
 
 
 def profile_enable(on: bool = True):
