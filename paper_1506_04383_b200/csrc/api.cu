@@ -240,10 +240,11 @@ bool use_sym(int32_t n, int dim) {
     if (!env) return false;
     const int64_t tb = (n + 1023) / 1024;
     if ((tb - 1) * (int64_t)n * stride_of(dim) * 4 > (int64_t(1) << 31)) return false;
-    // the triangular schedule has only TB(TB+1)/2 block-pair units: below ~4 per
-    // CTA its load imbalance costs more than the halved pair count saves
+    // the triangular schedule has 4 TB(TB+1)/2 units (block pair x source
+    // sub-tile): with fewer units than CTAs part of the GPU idles and the
+    // one-sided kernel is faster (measured: n = 16K already favours symmetric)
     const SymPlan sp = plan_repulse_sym(n, dim);
-    return env == 2 || sp.ts.U >= 4 * (int64_t)sp.ts.G;
+    return env == 2 || sp.ts.U >= sp.full_grid;
 }
 
 int part_slots(int32_t n, int dim, int32_t n_src, bool approx) {

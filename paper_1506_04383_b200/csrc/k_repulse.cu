@@ -312,14 +312,17 @@ __global__ void __launch_bounds__(WARPS * 32, MM_SYM_MINB) k_repulse_sym(int32_t
             Z[gg] = (DIM == 3) ? pk(__ldg(pa + 2), __ldg(pb + 2)) : 0ull;
             AX[gg] = AY[gg] = AZ[gg] = 0ull;
         }
+        // units of row I: (J, source sub-tile s) for J = I..TB-1, s = 0..NS-1
+        constexpr int NS = kSymTPB / SRC;
         for (; u < seg_end; ++u) {
-            const int32_t J = I + (int32_t)(u - pre);
+            const int32_t J = I + (int32_t)((u - pre) / NS);
+            const int s0 = (int)((u - pre) % NS) * SRC;
             const int64_t jblk = (int64_t)J * kSymTPB;
             const int jtot = (int)min((int64_t)kSymTPB, (int64_t)n - jblk);
-            // sources of J in sub-tiles of SRC (small shared footprint -> more resident warps)
-            for (int s0 = 0; s0 < jtot; s0 += SRC) {
+            {
                 const int64_t jbase = jblk + s0;
                 const int jcnt = min(SRC, jtot - s0);
+                if (jcnt <= 0) continue;  // sub-tiles past the end of the last block
                 __syncthreads();
                 for (int t = tid; t < SRC; t += NT)
                     src[t] = (t < jcnt) ? load_x<DIM>(x, jbase + t) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -662,9 +665,10 @@ cudaError_t sym_launch(int32_t n, const float* x, float cexp, const TriSched& ts
 SymPlan plan_repulse_sym(int32_t n, int dim) {
     SymPlan p;
     TriSched& t = p.ts;
+    // units: (block pair (I, J >= I), source sub-tile): row I has NS (TB - I)
     t.TB = (int32_t)((n + kSymTPB - 1) / kSymTPB);
-    t.Ub = t.TB;
-    t.c = 1;
+    t.Ub = t.TB * (kSymTPB / kSymSrc);
+    t.c = kSymTPB / kSymSrc;
     t.U = tri_prefix(t.TB, t);
     static int occ[2] = {0, 0};
     int& o = occ[dim == 3];
@@ -683,7 +687,8 @@ SymPlan plan_repulse_sym(int32_t n, int dim) {
         }
         o = std::max(v, 1);
     }
-    t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * o, t.U));
+    p.full_grid = (int64_t)sm_count() * o;
+    t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p.full_grid, t.U));
     int32_t ms = 1;
     for (int32_t I = 0; I < t.TB; ++I) {
         const int32_t a = sched_first_cta_tri(tri_prefix(I, t), t);

@@ -39,8 +39,9 @@ __host__ __device__ __forceinline__ int32_t sched_first_cta_tri(int64_t a, const
     return (int32_t)(((a + 1) * (int64_t)s.G - 1) / s.U);
 }
 struct SymPlan {
-    TriSched ts;   // blocks of 1024 vertices; units = block pairs (I, J >= I)
-    int slots = 1; // max i-side partial slots per vertex
+    TriSched ts;        // blocks of 1024 vertices; units = (block pair (I, J >= I), source sub-tile)
+    int slots = 1;      // max i-side partial slots per vertex
+    int64_t full_grid;  // resident CTAs of a full wave (148 x occupancy); ts.G = min(full_grid, U)
 };
 SymPlan plan_repulse_sym(int32_t n, int dim);
 int64_t sym_jpart_rows(const SymPlan& p);  // rows I of jpart[I][n] (blocks 0..TB-2)
