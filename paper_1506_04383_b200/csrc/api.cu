@@ -346,6 +346,11 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         ga.tri = sp.ts;
         ga.tpb = 1024;
     }
+    if (ap && !coarse_excludes_own()) {
+        ga.anc = ap->ancestor;
+        ga.rep_hi = sb.rep_hi;
+        ga.rep_lo = sb.rep_lo;
+    }
     ga.parent = ap ? ap->parent : nullptr;
     ga.child_ptr = ap ? sb.cptr : nullptr;
     ga.child = ap ? sb.child : nullptr;

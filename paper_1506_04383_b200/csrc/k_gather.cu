@@ -101,11 +101,17 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                     }
                 }
             }
-            const int64_t e0 = a.rp[i], e1 = a.rp[i + 1];
+            // row i: 64-bit base, 32-bit offsets; the S arrays are read once per
+            // sweep (streaming loads, evict-first) so that x stays in L2
+            const int64_t e0 = a.rp[i];
+            const int len = (int)(a.rp[i + 1] - e0);
+            const int32_t* __restrict__ colr = a.col + e0;
+            const float* __restrict__ dr = a.d + e0;
+            const float* __restrict__ wr = a.w + e0;
 #pragma unroll kGatherUnroll
-            for (int64_t e = e0 + lg; e < e1; e += G) {
-                const int32_t j = __ldg(a.col + e);
-                const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);
+            for (int k = lg; k < len; k += G) {
+                const int32_t j = __ldcs(colr + k);
+                const float dd = __ldcs(dr + k), ww = __ldcs(wr + k);
                 const float4 xj = load_x<DIM>(a.x, j);
                 const float dx = xi.x - xj.x, dy = xi.y - xj.y;
                 float r2 = fmaf(dx, dx, kEps2);
@@ -130,6 +136,25 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 if constexpr (DIM == 3) A.z = fmaf(ww, fmaf(s, dz, xj.z), A.z);
                 const float dev = dist - dd;
                 st = fmaf(ww * dev, dev, st);
+            }
+            if (a.anc != nullptr && lg == 0) {
+                // Eq.(3) excludes the own representative H(i); kernel (c)
+                // summed all k, so its term goes into C (subtracted), computed with
+                // kernel (c)'s hi/lo differencing (Q25)
+                const int32_t h = __ldg(a.anc + i);
+                const float4 rh = __ldg(a.rep_hi + h), rl = __ldg(a.rep_lo + h);
+                const float dx = (xi.x - rh.x) - rl.x, dy = (xi.y - rh.y) - rl.y;
+                float r2 = fmaf(dx, dx, kEps2);
+                r2 = fmaf(dy, dy, r2);
+                float dz = 0.f;
+                if constexpr (DIM == 3) {
+                    dz = (xi.z - rh.z) - rl.z;
+                    r2 = fmaf(dz, dz, r2);
+                }
+                const float inv = inv_pow<QPOW>(r2, cexp) * rh.w;
+                C.x = fmaf(dx, inv, C.x);
+                C.y = fmaf(dy, inv, C.y);
+                if constexpr (DIM == 3) C.z = fmaf(dz, inv, C.z);
             }
             if (a.parent != nullptr) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
                 const int32_t p = __ldg(a.parent + i);
@@ -340,10 +365,14 @@ int gather_blocks(int32_t n, double mean_row) {
     const int64_t need = ((int64_t)n * G + kGBlock - 1) / kGBlock;
     static int cap = 0;
     if (!cap) {
-        int dev = 0, sms = 148, occ = 6;
+        int dev = 0, sms = 148, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cap = sms * occ * 2;  // a few resident waves of grid-stride CTAs
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<2, false, 8>, kGBlock, 0);
+        if (occ <= 0) occ = MM_GATHER_MINB;
+        const char* e = getenv("MM_GATHER_WAVES");  // experiments
+        const int waves = e ? std::max(1, atoi(e)) : 2;
+        cap = sms * occ * waves;  // a few resident waves of grid-stride CTAs
     }
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
 }

@@ -5,9 +5,10 @@
 //     over ALL vertices (the second term of Eq.(2), with the
 //     exponent q of BASELINE.json's north_star).  Kernel (a) afterwards
 //     subtracts the S_i pairs, so the net sum runs over j notin S_i.
-// (c) computes sum_{v' != H(i)} nu(v') (x_i - x'_v')/|x_i - x'_v'|^(q+2), the
-//     representative term of Eq.(3), over the k coarse
-//     representatives {x', nu} of the approximation level.
+// (c) computes sum_{v'} nu(v') (x_i - x'_v')/|x_i - x'_v'|^(q+2) over ALL k
+//     coarse representatives {x', nu} of the approximation level; kernel (a)
+//     subtracts the own representative's term, so the net sum is Eq.(3)'s
+//     sum over v' != H(i) (Q25).
 //
 // Design (B200, sm_100a): n-body tiling.  A work item is (target block of
 // 256*T targets, source tile of 256 sources); targets live in registers (T per
@@ -50,6 +51,9 @@ __device__ __forceinline__ f2x inv_pair(f2x r2, float cexp) {
     }
 }
 
+#ifndef MM_COARSE_MASK
+#define MM_COARSE_MASK 0  // 1: exclude H(i) inside kernel (c) (experiments; round-1 design)
+#endif
 template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4>
 __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
                                                     const float4* __restrict__ rep_hi,
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             Y[gg] = pk(__ldg(pa + 1), __ldg(pb + 1));
             Z[gg] = (DIM == 3) ? pk(__ldg(pa + 2), __ldg(pb + 2)) : 0ull;
             AX[gg] = AY[gg] = AZ[gg] = 0ull;
-            if constexpr (COARSE) {
+            if constexpr (COARSE && MM_COARSE_MASK) {
                 hi[2 * gg] = __ldg(anc + ca);
                 hi[2 * gg + 1] = __ldg(anc + cb);
             }
@@ -147,8 +151,23 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
                         r2 = fma2(dz, dz, r2);
                     }
                     // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
-                    f2x inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
-                    if constexpr (COARSE) {
+                    f2x inv;
+                    if constexpr (COARSE && !MM_COARSE_MASK) {
+                        // all k representatives, the own one H(i) included: kernel (a)
+                        // subtracts that term (Q25); nu folded into the
+                        // batched reciprocal: nu/a = b * (nu * rcp(ab))
+                        if ((BMASK >> gg) & 1) {
+                            float r0, r1;
+                            upk(r2, r0, r1);
+                            const float ip = nu * rcp_approx(r0 * r1);
+                            inv = mul_bc(pk(r1, r0), ip);
+                        } else {
+                            inv = mul_bc(inv_pair<QPOW, false>(r2, cexp), nu);
+                        }
+                    } else {
+                        inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+                    }
+                    if constexpr (COARSE && MM_COARSE_MASK) {
                         const int32_t j = (int32_t)(t0 + jj);
                         inv = mul2(inv, pk(j == hi[2 * gg] ? 0.f : nu, j == hi[2 * gg + 1] ? 0.f : nu));
                     }
@@ -644,6 +663,8 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
 }
 
 int repulse_targets_per_block(int dim) { return kBlock * targets_per_thread(dim); }
+
+bool coarse_excludes_own() { return MM_COARSE_MASK != 0; }
 
 namespace {
 template <int DIM, bool QPOW>

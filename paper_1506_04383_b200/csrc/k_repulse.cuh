@@ -54,6 +54,7 @@ struct EntropyPlan {
 
 RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, bool qpow);
 int repulse_targets_per_block(int dim);
+bool coarse_excludes_own();  // kernel (c) built with MM_COARSE_MASK = 1
 cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_tgt, const float* x,
                            int32_t n_src, const float4* rep_hi, const float4* rep_lo, const int32_t* anc,
                            const RepulsePlan& p, float* part, cudaStream_t st);
@@ -78,6 +79,12 @@ struct GatherArgs {
     // schedule `tri`; jpart[I][i] for I < block(i) holds the j-side sums
     const float* jpart = nullptr;  // nullable: rectangular schedule
     TriSched tri;
+    // Eq.(3) own-representative term, subtracted because kernel (c) sums over
+    // all k representatives (nullable: exact mode, or kernel (c) built with
+    // MM_COARSE_MASK = 1)
+    const int32_t* anc = nullptr;
+    const float4* rep_hi = nullptr;
+    const float4* rep_lo = nullptr;
     // Eq.(3) sibling term (nullable: exact mode)
     const int32_t* parent;
     const int32_t* child_ptr;

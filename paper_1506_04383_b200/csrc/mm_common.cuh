@@ -69,6 +69,12 @@ __device__ __forceinline__ f2x sub_bc(f2x a, float s) {
     asm("{.reg .b64 t; mov.b64 t, {%2,%2}; sub.rn.f32x2 %0, %1, t;}" : "=l"(d) : "l"(a), "f"(s));
     return d;
 }
+// a * (s, s): FMUL2 with a broadcast scalar operand
+__device__ __forceinline__ f2x mul_bc(f2x a, float s) {
+    f2x d;
+    asm("{.reg .b64 t; mov.b64 t, {%2,%2}; mul.rn.f32x2 %0, %1, t;}" : "=l"(d) : "l"(a), "f"(s));
+    return d;
+}
 __device__ __forceinline__ f2x add2(f2x a, f2x b) {
     f2x d;
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));

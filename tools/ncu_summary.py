@@ -25,7 +25,7 @@ for r in rows[2:]:
         if k in d:
             print(f"  {k:62s} {d[k]:>16s} {u[h.index(k)]}")
     stalls = [(k, float(d[k].replace(",", ""))) for k in h
-              if k.startswith("smsp__average_warp_latency_issue_stalled") and k.endswith(".ratio") and d[k]]
+              if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("_per_issue_active.ratio") and d[k]]
     stalls.sort(key=lambda t: -t[1])
     print("  top stall reasons (cycles per issued instruction):",
-          ", ".join(f"{k.split('stalled_')[1].replace('.ratio', '')}={v:.2f}" for k, v in stalls[:6]))
+          ", ".join(f"{k.split('stalled_')[1].replace('_per_issue_active.ratio', '')}={v:.2f}" for k, v in stalls[:6]))
