@@ -371,8 +371,8 @@ int gather_blocks(int32_t n, double mean_row) {
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<2, false, 8>, kGBlock, 0);
         if (occ <= 0) occ = MM_GATHER_MINB;
         const char* e = getenv("MM_GATHER_WAVES");  // experiments
-        const int waves = e ? std::max(1, atoi(e)) : 2;
-        cap = sms * occ * waves;  // a few resident waves of grid-stride CTAs
+        const int waves = e ? std::max(1, atoi(e)) : 1;
+        cap = sms * occ * waves;  // one resident wave of grid-stride CTAs (measured best: r01_gather_groups.txt)
     }
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
 }
