@@ -440,6 +440,8 @@ constexpr int kSymWarps = kSymTPB / (64 * kSymSG);
 // from its own first tile on; the unit space is split into G equal ranges and
 // every CTA writes one FP64 partial (FP32 within a tile, FP64 across tiles).
 constexpr float kR2Floor = 1e-18f;  // r^2 clamp: keeps products of two r^2 normal
+constexpr uint32_t kP4Lo = 0x0d800000u;  // 2^-100: bit patterns of the accepted product range
+constexpr uint32_t kP4Hi = 0x7e800000u;  // 2^126
 
 template <int DIM>
 __device__ __forceinline__ f2x entropy_r2(f2x X, f2x Y, f2x Z, const float4& sv) {
@@ -515,7 +517,38 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
             const bool diag = (t0 < base + TPB) || (base + TPB > n);
             float acc = 0.f;
             int32_t zt = 0;
-            if (!diag) {
+            if (!diag && !QPOW) {
+                // q = 0: lg2 of the product of the four r^2 of one source (one MUFU
+                // per 4 pairs) when that product is a normal float in
+                // [2^-100, 2^126]; a thread that saw any other product (coincident,
+                // tiny or huge r^2) redoes its tile pair by pair (branch-free hot loop)
+                bool bad = false;
+#pragma unroll 4
+                for (int jj = 0; jj < cnt; ++jj) {
+                    const float4 sv = sm[jj];
+                    const f2x r0 = entropy_r2<DIM>(X[0], Y[0], Z[0], sv), r1 = entropy_r2<DIM>(X[1], Y[1], Z[1], sv);
+                    float pa, pb;
+                    upk(mul2(r0, r1), pa, pb);
+                    const float p4 = pa * pb;
+                    const bool ok = (__float_as_uint(p4) - kP4Lo) < (kP4Hi - kP4Lo);
+                    const float l = lg2_approx(p4);
+                    acc += ok ? l : 0.f;
+                    bad |= !ok;
+                }
+                if (bad) {
+                    acc = 0.f;
+                    for (int jj = 0; jj < cnt; ++jj) {
+                        const float4 sv = sm[jj];
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) {
+                            float ra, rb;
+                            upk(entropy_r2<DIM>(X[gg], Y[gg], Z[gg], sv), ra, rb);
+                            zt += (ra == 0.f) + (rb == 0.f);
+                            acc += entropy_phi2<false>(fmaxf(ra, kR2Floor), fmaxf(rb, kR2Floor), cq);
+                        }
+                    }
+                }
+            } else if (!diag) {
 #pragma unroll 4
                 for (int jj = 0; jj < cnt; ++jj) {
                     const float4 sv = sm[jj];

@@ -63,6 +63,42 @@ def test_energy_coincident_error(mm):
     assert ei.value.status == -3
 
 
+def _extreme_points(n=4096, seed=7):
+    """Typical points plus tight pairs (r^2 ~ 1e-12) and far points (r^2 ~ 1e12):
+    products of four r^2 leave [2^-100, 2^126], so kernel (e)'s per-pair path runs
+    inside the far (non-diagonal) tiles as well as the one-MUFU-per-4-pairs path."""
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(0.0, 64.0, size=(n, 2))
+    tight = rng.choice(n, 400, replace=False)
+    x[tight[:200]] = rng.uniform(0.0, 0.01, size=(200, 2))
+    x[tight[200:]] = x[tight[:200]] + np.array([1e-6, 0.0])
+    far = rng.choice(np.setdiff1d(np.arange(n), tight), 300, replace=False)
+    x[far] = rng.uniform(-1e6, 1e6, size=(300, 2))
+    return x.astype(np.float32)
+
+
+def test_energy_extreme_scales(mm):
+    n = 4096
+    x = _extreme_points(n)
+    g = H.path(n)
+    S = H.sset_with(g, np.ones(g.nnz))
+    e = mm.energy(mm.sset_to_device(S), mm.coords_to_device(x), 0.01, 0.0)
+    o = oracle.energy(S, x.astype(np.float64), 0.01, 0.0)
+    assert _rel(e[1], o[1]) <= 1e-4, (e, o)
+
+
+def test_energy_coincident_far_tile_error(mm):
+    """An exactly coincident non-S pair whose vertices lie in different tiles."""
+    n = 4096
+    x = _extreme_points(n)
+    x[n - 5] = x[3]
+    g = H.path(n)
+    S = H.sset_with(g, np.ones(g.nnz))
+    with pytest.raises(mm.MMError) as ei:
+        mm.energy(mm.sset_to_device(S), mm.coords_to_device(x), 0.01, 0.0)
+    assert ei.value.status == -3
+
+
 def test_layout_exact_cfg1_full_run(mm):
     """configs[0] exactly as specified: 50 exact sweeps from the seeded start."""
     w = workload("cfg1")
