@@ -740,7 +740,7 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
         for (int32_t r = 0; r < max_rounds; ++r) {
             int32_t h_added = 0;
             if (cudaMemsetAsync(added, 0, 4, st) ||
-                run_match_round(cur.n, cur.rp, cur.col, cur.omega, cur.c, mate, cand, seed, (int32_t)li, r, added, st) ||
+                run_match_round(cur.n, cur.nnz, cur.rp, cur.col, cur.omega, cur.c, mate, cand, seed, (int32_t)li, r, added, st) ||
                 cudaMemcpyAsync(&h_added, added, 4, cudaMemcpyDeviceToHost, st) || cudaStreamSynchronize(st)) {
                 cudaError_t e = cudaGetLastError();
                 set_err("mm_build_hierarchy: matching round failed: %s", cudaGetErrorString(e));
@@ -801,7 +801,7 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
             (m2 > 0 && cudaMemcpyAsync(nx.col, ccol, 4 * m2, cudaMemcpyDeviceToDevice, st)) ||
             (m2 > 0 && cudaMemcpyAsync(nx.omega, comega, 4 * m2, cudaMemcpyDeviceToDevice, st)) ||
             cudaMemcpyAsync(nx.c, cnext, 4 * (size_t)nc, cudaMemcpyDeviceToDevice, st) ||
-            launch_coarse_sset(nc, nx.rp, nx.col, nx.c, dim, nx.d, nx.w, st)) {
+            launch_coarse_sset(m2, vals, nx.col, nx.c, dim, nx.d, nx.w, st)) {
             set_err("mm_build_hierarchy: level assembly failed: %s", cudaGetErrorString(cudaGetLastError()));
             return fail(MM_ERR_CUDA);
         }

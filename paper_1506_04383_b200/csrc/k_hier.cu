@@ -51,36 +51,38 @@ __device__ __forceinline__ bool cand_better(const Cand& a, const Cand& b) {
     return a.v < b.v;
 }
 
-// One warp per vertex: lanes scan the row strided, then a shuffle reduction
-// under the (total) candidate order picks the best unmatched neighbour.
+// G lanes per vertex (G from the mean degree): the group scans the row
+// strided, then a shuffle reduction under the (total) candidate order picks
+// the best unmatched neighbour.  All lanes reach the shuffles.
+template <int G>
 __global__ void k_match_pick(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
                              const int32_t* __restrict__ omega, const int32_t* __restrict__ c,
                              const int32_t* __restrict__ mate, int32_t* __restrict__ cand, uint64_t seed,
                              int32_t level, int32_t round) {
-    const int32_t u = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
-    const int lane = threadIdx.x & 31;
-    if (u >= n) return;  // whole warp exits together
-    if (mate[u] >= 0) {
-        if (lane == 0) cand[u] = -1;
-        return;
-    }
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t u = (int32_t)(t / G);
+    const int lg = (int)(t & (G - 1));
     Cand best{-1, 0, 1, 0};
-    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
-        const int32_t v = col[e];
-        if (v == u || mate[v] >= 0) continue;
-        const Cand cv{v, omega ? omega[e] : 1, c[v], match_hash(seed, level, round, u, v)};
-        if (cand_better(cv, best)) best = cv;
+    const bool active = u < n && mate[u] < 0;
+    if (active) {
+        const int64_t e1 = rp[u + 1];
+        for (int64_t e = rp[u] + lg; e < e1; e += G) {
+            const int32_t v = col[e];
+            if (v == u || mate[v] >= 0) continue;
+            const Cand cv{v, omega ? omega[e] : 1, c[v], match_hash(seed, level, round, u, v)};
+            if (cand_better(cv, best)) best = cv;
+        }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
+    for (int o = G / 2; o > 0; o >>= 1) {
         Cand other;
-        other.v = __shfl_xor_sync(0xffffffffu, best.v, o);
-        other.w = __shfl_xor_sync(0xffffffffu, best.w, o);
-        other.c = __shfl_xor_sync(0xffffffffu, best.c, o);
-        other.h = __shfl_xor_sync(0xffffffffu, best.h, o);
+        other.v = __shfl_xor_sync(0xffffffffu, best.v, o, G);
+        other.w = __shfl_xor_sync(0xffffffffu, best.w, o, G);
+        other.c = __shfl_xor_sync(0xffffffffu, best.c, o, G);
+        other.h = __shfl_xor_sync(0xffffffffu, best.h, o, G);
         if (cand_better(other, best)) best = other;
     }
-    if (lane == 0) cand[u] = best.v;
+    if (u < n && lg == 0) cand[u] = active ? best.v : -1;
 }
 
 __global__ void k_match_confirm(int32_t n, const int32_t* __restrict__ cand, int32_t* __restrict__ mate,
@@ -119,18 +121,25 @@ __global__ void k_parent(int32_t n, const int32_t* __restrict__ mate, const int3
 
 // keys (parent[u] * nc + parent[v]) for crossing entries; intra-cluster -> sentinel nc*nc
 // (one warp per row: coarse Chung-Lu levels have rows of 10^4-10^5 entries)
-__global__ void k_edge_keys(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
-                            const int32_t* __restrict__ omega, const int32_t* __restrict__ parent, int64_t nc,
-                            uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+// row id of every CSR entry: one warp per row writes u over [rp[u], rp[u+1])
+// (stores only, so heavy rows cost little)
+__global__ void k_row_ids(int32_t n, const int64_t* __restrict__ rp, int32_t* __restrict__ row) {
     const int32_t u = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int lane = threadIdx.x & 31;
     if (u >= n) return;
-    const int64_t pu = parent[u];
-    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
-        const int64_t pv = parent[col[e]];
-        keys[e] = (pu != pv) ? (uint64_t)(pu * nc + pv) : (uint64_t)(nc * nc);
-        vals[e] = omega ? omega[e] : 1;
-    }
+    const int64_t e1 = rp[u + 1];
+    for (int64_t e = rp[u] + lane; e < e1; e += 32) row[e] = u;
+}
+
+// edge-parallel: key = parent(u) * nc + parent(v) for crossing entries, sentinel nc^2 otherwise
+__global__ void k_edge_keys(int64_t m, const int32_t* __restrict__ row, const int32_t* __restrict__ col,
+                            const int32_t* __restrict__ omega, const int32_t* __restrict__ parent, int64_t nc,
+                            uint64_t* __restrict__ keys, int32_t* __restrict__ vals) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const int64_t pu = __ldg(parent + __ldg(row + e)), pv = __ldg(parent + __ldg(col + e));
+    keys[e] = (pu != pv) ? (uint64_t)(pu * nc + pv) : (uint64_t)(nc * nc);
+    vals[e] = omega ? __ldg(omega + e) : 1;
 }
 
 __global__ void k_run_heads(int64_t m, const uint64_t* __restrict__ keys, uint64_t sentinel, int32_t* __restrict__ head) {
@@ -167,19 +176,18 @@ __global__ void k_rowptr_search(int32_t nc, const int32_t* __restrict__ urow, in
     rp[p] = lo;
 }
 
-__global__ void k_coarse_sset(int32_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ col,
+// coarse S^l = E^l (Q7), edge-parallel over the m2 unique entries: d = s(c_u) + s(c_v),
+// s(c) = c^(1/dim), w = d^-2
+__global__ void k_coarse_sset(int64_t m, const int32_t* __restrict__ urow, const int32_t* __restrict__ col,
                               const int32_t* __restrict__ c, int dim, float* __restrict__ d, float* __restrict__ w) {
-    const int32_t u = (int32_t)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);  // warp per row
-    const int lane = threadIdx.x & 31;
-    if (u >= n) return;
-    const float su = dim == 2 ? sqrtf((float)c[u]) : cbrtf((float)c[u]);
-    for (int64_t e = rp[u] + lane; e < rp[u + 1]; e += 32) {
-        const int32_t v = col[e];
-        const float sv = dim == 2 ? sqrtf((float)c[v]) : cbrtf((float)c[v]);
-        const float dd = su + sv;
-        d[e] = dd;
-        w[e] = 1.0f / (dd * dd);
-    }
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= m) return;
+    const float cu = (float)__ldg(c + __ldg(urow + e)), cv = (float)__ldg(c + __ldg(col + e));
+    const float su = dim == 2 ? sqrtf(cu) : cbrtf(cu);
+    const float sv = dim == 2 ? sqrtf(cv) : cbrtf(cv);
+    const float dd = su + sv;
+    d[e] = dd;
+    w[e] = 1.0f / (dd * dd);
 }
 
 __global__ void k_iota(int32_t n, int32_t* __restrict__ a) {
@@ -323,16 +331,39 @@ __global__ void k_sum_f32(int64_t m, const float* __restrict__ a, double* __rest
 
 inline int nblk(int64_t n, int b = 256) { return (int)((n + b - 1) / b); }
 
+// lanes per vertex for the matching scan: about 2 row entries per lane
+// (MM_MATCH_G overrides, experiments)
+int match_group(int32_t n, int64_t nnz) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* e = getenv("MM_MATCH_G");
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
+    const double mean = n > 0 ? (double)nnz / n : 0.0;
+    int g = 2;
+    while (g < 32 && 2.0 * (2 * g) <= mean) g *= 2;
+    return g;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host side
 
-cudaError_t run_match_round(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* omega,
+cudaError_t run_match_round(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
                             const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
                             int32_t round, int32_t* added, cudaStream_t st) {
     {
         LaunchScope ls("match_pick", st);
-        k_match_pick<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round);
+        const int G = match_group(n, nnz);
+        const int nb = nblk((int64_t)n * G);
+        switch (G) {
+            case 2: k_match_pick<2><<<nb, 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round); break;
+            case 4: k_match_pick<4><<<nb, 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round); break;
+            case 8: k_match_pick<8><<<nb, 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round); break;
+            case 16: k_match_pick<16><<<nb, 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round); break;
+            default: k_match_pick<32><<<nb, 256, 0, st>>>(n, rp, col, omega, c, mate, cand, seed, level, round); break;
+        }
     }
     {
         LaunchScope ls("match_confirm", st);
@@ -393,8 +424,13 @@ cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int3
                            int32_t* comega_tmp, int32_t* rowcnt, void* tmp, size_t tmp_bytes, cudaStream_t st) {
     cudaError_t e;
     {
+        // head is free until run_heads: it carries the row id of every entry
+        LaunchScope ls("row_ids", st);
+        k_row_ids<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, head);
+    }
+    {
         LaunchScope ls("edge_keys", st);
-        k_edge_keys<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, col, omega, parent, nc, keys, vals);
+        k_edge_keys<<<nblk(nnz), 256, 0, st>>>(nnz, head, col, omega, parent, nc, keys, vals);
     }
     const uint64_t sentinel = (uint64_t)nc * (uint64_t)nc;
     int end_bit = 1;
@@ -423,10 +459,11 @@ cudaError_t rowptr_from_rows(int32_t nc, const int32_t* urow, int64_t m2, int64_
     return cudaGetLastError();
 }
 
-cudaError_t launch_coarse_sset(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* c, int dim,
+cudaError_t launch_coarse_sset(int64_t m, const int32_t* urow, const int32_t* col, const int32_t* c, int dim,
                                float* d, float* w, cudaStream_t st) {
+    if (m <= 0) return cudaSuccess;
     LaunchScope ls("coarse_sset", st);
-    k_coarse_sset<<<nblk((int64_t)n * 32), 256, 0, st>>>(n, rp, col, c, dim, d, w);
+    k_coarse_sset<<<nblk(m), 256, 0, st>>>(m, urow, col, c, dim, d, w);
     return cudaGetLastError();
 }
 

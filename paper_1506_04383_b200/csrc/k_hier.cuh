@@ -4,7 +4,7 @@
 
 namespace mm {
 
-cudaError_t run_match_round(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* omega,
+cudaError_t run_match_round(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
                             const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
                             int32_t round, int32_t* added, cudaStream_t st);
 cudaError_t launch_fill(int64_t n, int32_t v, int32_t* a, cudaStream_t st);
@@ -21,7 +21,8 @@ cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int3
                            int32_t* comega_tmp, int32_t* rowcnt, void* tmp, size_t tmp_bytes, cudaStream_t st);
 // coarse row_ptr from the row ids of the m2 unique entries (written into `vals` by contract_edges)
 cudaError_t rowptr_from_rows(int32_t nc, const int32_t* urow, int64_t m2, int64_t* rp, cudaStream_t st);
-cudaError_t launch_coarse_sset(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* c, int dim,
+// coarse S^l distances / weights (Q7), edge-parallel over the m unique entries with row ids urow
+cudaError_t launch_coarse_sset(int64_t m, const int32_t* urow, const int32_t* col, const int32_t* c, int dim,
                                float* d, float* w, cudaStream_t st);
 cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr, int32_t* members,
                          int32_t* key_sorted, int32_t* iota, int32_t* cnt, void* tmp, size_t tmp_bytes,
