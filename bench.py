@@ -166,6 +166,39 @@ def cpu_oracle_sample(w, target_s: float = 8.0, max_rows=None):
     return rows, cores
 
 
+def oracle_approx_setup(w):
+    """Multilevel configs: the oracle's own hierarchy (FP64 C, test infrastructure)
+    and the finest level's Eq.(3) map (parent, ancestor at level h, k), with a
+    seeded random state of the layout's scale."""
+    import numpy as np
+
+    import oracle
+    from workloads import configs
+
+    lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=1000)
+    h = min(w.h, len(lv) - 1)
+    anc = oracle.ancestor(lv, 0, h)
+    x = configs.random_state(w.n, w.dim, seed=1, scale=w.n ** (1.0 / w.dim)).astype(np.float64)
+    return lv[0].parent, anc, lv[h].n, x
+
+
+def cpu_oracle_sample_approx(w, setup, target_s: float = 8.0):
+    """Bounded row sample of one finest-level Eq.(3) sweep, sized from a calibration run."""
+    import numpy as np
+
+    import oracle
+
+    parent, anc, k, x = setup
+    cores = oracle.default_threads()
+    rng = np.random.default_rng(0)
+    calib = np.sort(rng.choice(w.n, size=min(w.n, 64 * cores), replace=False)).astype(np.int32)
+    t0 = time.perf_counter()
+    oracle.sweep_approx(w.S, x, w.alpha, w.q, parent, anc, k, rows=calib, nthreads=cores)
+    rate = calib.shape[0] / max(time.perf_counter() - t0, 1e-9)
+    rows_n = int(min(w.n, max(calib.shape[0], rate * target_s)))
+    return np.sort(rng.choice(w.n, size=rows_n, replace=False)).astype(np.int32), cores
+
+
 def run_reference(args):
     """--impl reference: the FP64 oracle on the host cores (rank 0 only)."""
     ws, rank, _ = dist_env()
@@ -176,26 +209,42 @@ def run_reference(args):
     import oracle
 
     w = load_workload(args.config)
-    rows, cores = cpu_oracle_sample(w, target_s=args.ref_step_s)
-    x = w.x0.astype(np.float64)
+    if w.h == 0:
+        rows, cores = cpu_oracle_sample(w, target_s=args.ref_step_s)
+        x = w.x0.astype(np.float64)
+
+        def one(r):
+            oracle.sweep_exact(w.S, x, w.alpha, w.q, rows=r, nthreads=cores)
+
+        sample = (f"{rows.shape[0]} of {w.n} rows of one exact Eq.(2) sweep of {args.config} per step "
+                  f"(each row: |S_i| gathers + {w.n - 1} pair terms, FP64)")
+    else:
+        setup = oracle_approx_setup(w)
+        rows, cores = cpu_oracle_sample_approx(w, setup, target_s=args.ref_step_s)
+        parent, anc, k, x = setup
+
+        def one(r):
+            oracle.sweep_approx(w.S, x, w.alpha, w.q, parent, anc, k, rows=r, nthreads=cores)
+
+        sample = (f"{rows.shape[0]} of {w.n} rows of one finest-level Eq.(3) sweep of {args.config} per step "
+                  f"(k = {k} representatives of level {w.h}, oracle hierarchy, FP64; the centroids are "
+                  f"recomputed from all n vertices in every call)")
     for _ in range(args.warmup):
-        oracle.sweep_exact(w.S, x, w.alpha, w.q, rows=rows[: max(1, rows.shape[0] // 8)], nthreads=cores)
+        one(rows[: max(1, rows.shape[0] // 8)])
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        oracle.sweep_exact(w.S, x, w.alpha, w.q, rows=rows, nthreads=cores)
+        one(rows)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = rows.shape[0] * args.steps / tot
-    sample = (f"{rows.shape[0]} of {w.n} rows of one exact Eq.(2) sweep of {args.config} per step "
-              f"(each row: |S_i| gathers + {w.n - 1} pair terms, FP64)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": config_block(w, args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "pair_interactions_per_s": value * (w.n - 1)}
+            "pair_interactions_per_s": value * (w.n - 1) if w.h == 0 else None}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -372,6 +421,18 @@ def run_gpu(args):
         cpu = {"value": rows.shape[0] / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
                "sample": f"{rows.shape[0]} of {n} rows of one exact Eq.(2) sweep of {w.name} "
                          f"(FP64, OpenMP over rows), {dt:.1f} s"}
+    elif ws == 1 and not args.no_cpu_baseline and not args.schedule:
+        import oracle
+
+        setup = oracle_approx_setup(w)
+        rows, cores = cpu_oracle_sample_approx(w, setup, target_s=args.cpu_s)
+        parent, anc, k, x = setup
+        t0 = time.perf_counter()
+        oracle.sweep_approx(w.S, x, w.alpha, w.q, parent, anc, k, rows=rows, nthreads=cores)
+        dt = time.perf_counter() - t0
+        cpu = {"value": rows.shape[0] / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+               "sample": f"{rows.shape[0]} of {n} rows of one finest-level Eq.(3) sweep of {w.name} "
+                         f"(k = {k}, oracle hierarchy; FP64, OpenMP over rows), {dt:.1f} s"}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
