@@ -54,15 +54,16 @@ void* g_alloc_ctx = nullptr;
 // threshold 0 returns them to the driver at every synchronisation, and the
 // next cudaMallocAsync would map fresh pages).
 void keep_pool_warm() {
-    static bool done = false;
-    if (done) return;
-    done = true;
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-        uint64_t thr = UINT64_MAX;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
+    static const bool done = [] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        return true;
+    }();
+    (void)done;
     cudaGetLastError();
 }
 
@@ -115,12 +116,11 @@ struct DevBuf {
 
 // ------------------------------------------------------------------ host trace (MM_TRACE=1)
 bool trace_on() {
-    static int on = -1;
-    if (on < 0) {
+    static const bool on = [] {
         const char* e = getenv("MM_TRACE");
-        on = (e && e[0] && e[0] != '0') ? 1 : 0;
-    }
-    return on == 1;
+        return e && e[0] && e[0] != '0';
+    }();
+    return on;
 }
 void trace(const char* what) {
     if (!trace_on()) return;
@@ -232,11 +232,10 @@ size_t cub_tmp_bytes(int32_t n) {
 // unless MM_SYM=0, its j-side buffer would exceed 2 GiB, or the triangular
 // schedule has too few units per CTA; MM_SYM=2 forces it (tests).
 bool use_sym(int32_t n, int dim) {
-    static int env = -1;
-    if (env < 0) {
+    static const int env = [] {
         const char* v = getenv("MM_SYM");
-        env = (v && v[0] == '0') ? 0 : (v && v[0] == '2') ? 2 : 1;  // 2: force (tests)
-    }
+        return (v && v[0] == '0') ? 0 : (v && v[0] == '2') ? 2 : 1;  // 2: force (tests)
+    }();
     if (!env) return false;
     const int64_t tb = (n + 1023) / 1024;
     if ((tb - 1) * (int64_t)n * stride_of(dim) * 4 > (int64_t(1) << 31)) return false;

@@ -345,11 +345,10 @@ __global__ void __launch_bounds__(kGBlock) k_energy_s(int32_t n, const int64_t* 
 }
 
 int pick_group(double mean_row) {
-    static int forced = -1;
-    if (forced < 0) {
+    static const int forced = [] {
         const char* e = getenv("MM_GATHER_G");  // experiments: 1, 2, 4, 8, 16, 32
-        forced = e ? atoi(e) : 0;
-    }
+        return e ? atoi(e) : 0;
+    }();
     if (forced == 1 || forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     // about 8 row entries per lane: more independent loads in flight per lane
     // beat wider groups (tools/bench_gather.py sweep, profiles/r01_gather_groups.txt)
@@ -363,8 +362,7 @@ int pick_group(double mean_row) {
 int gather_blocks(int32_t n, double mean_row) {
     const int G = pick_group(mean_row);
     const int64_t need = ((int64_t)n * G + kGBlock - 1) / kGBlock;
-    static int cap = 0;
-    if (!cap) {
+    static const int cap = [] {
         int dev = 0, sms = 148, occ = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -372,8 +370,8 @@ int gather_blocks(int32_t n, double mean_row) {
         if (occ <= 0) occ = MM_GATHER_MINB;
         const char* e = getenv("MM_GATHER_WAVES");  // experiments
         const int waves = e ? std::max(1, atoi(e)) : 1;
-        cap = sms * occ * waves;  // one resident wave of grid-stride CTAs (measured best: r01_gather_groups.txt)
-    }
+        return sms * occ * waves;  // one resident wave of grid-stride CTAs (measured best: r01_gather_groups.txt)
+    }();
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
 }
 

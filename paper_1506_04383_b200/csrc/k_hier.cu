@@ -334,11 +334,10 @@ inline int nblk(int64_t n, int b = 256) { return (int)((n + b - 1) / b); }
 // lanes per vertex for the matching scan: about 2 row entries per lane
 // (MM_MATCH_G overrides, experiments)
 int match_group(int32_t n, int64_t nnz) {
-    static int forced = -1;
-    if (forced < 0) {
+    static const int forced = [] {
         const char* e = getenv("MM_MATCH_G");
-        forced = e ? atoi(e) : 0;
-    }
+        return e ? atoi(e) : 0;
+    }();
     if (forced == 2 || forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
     const double mean = n > 0 ? (double)nnz / n : 0.0;
     int g = 2;

@@ -616,23 +616,24 @@ constexpr int kBatchMask = (DIM == 2 && !QPOW) ? 1 : 0;  // measured: tools/uben
 
 template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
-    static int occ = 0;  // per instantiation; queried once
-    if (!occ) {
+    static const int occ = [] {  // per instantiation; queried once
         int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>>,
                                                       kBlock, 0);
-        occ = o > 0 ? o : 1;
-    }
+        return o > 0 ? o : 1;
+    }();
     return occ;
 }
 
+// lazily queried device properties: function-local statics (thread-safe
+// initialisation; one process drives one GPU)
 int sm_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
+    static const int sms = [] {
+        int dev = 0, v = 0;
         cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    }
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        return v;
+    }();
     return sms;
 }
 
@@ -705,11 +706,8 @@ cudaError_t sym_launch(int32_t n, const float* x, float cexp, const TriSched& ts
                        cudaStream_t st) {
     constexpr int smem = sym_smem_bytes<DIM>(kSymWarps);
     auto* fn = k_repulse_sym<DIM, QPOW, kSymSG, kSymWarps, kSymSrc>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr = true;
-    }
+    static const bool attr = (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem), true);
+    (void)attr;
     fn<<<ts.G, kSymWarps * 32, smem, st>>>(n, x, cexp, ts, ipart, jpart);
     return cudaGetLastError();
 }
@@ -724,23 +722,23 @@ SymPlan plan_repulse_sym(int32_t n, int dim) {
     t.Ub = t.TB * (kSymTPB / kSymSrc);
     t.c = kSymTPB / kSymSrc;
     t.U = tri_prefix(t.TB, t);
-    static int occ[2] = {0, 0};
-    int& o = occ[dim == 3];
-    if (!o) {
+    static const int occ2 = [] {
         int v = 0;
-        if (dim == 2) {
-            cudaFuncSetAttribute(k_repulse_sym<2, false, kSymSG, kSymWarps, kSymSrc>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem_bytes<2>(kSymWarps));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_repulse_sym<2, false, kSymSG, kSymWarps, kSymSrc>,
-                                                          kSymWarps * 32, sym_smem_bytes<2>(kSymWarps));
-        } else {
-            cudaFuncSetAttribute(k_repulse_sym<3, false, kSymSG, kSymWarps, kSymSrc>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem_bytes<3>(kSymWarps));
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_repulse_sym<3, false, kSymSG, kSymWarps, kSymSrc>,
-                                                          kSymWarps * 32, sym_smem_bytes<3>(kSymWarps));
-        }
-        o = std::max(v, 1);
-    }
+        cudaFuncSetAttribute(k_repulse_sym<2, false, kSymSG, kSymWarps, kSymSrc>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem_bytes<2>(kSymWarps));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_repulse_sym<2, false, kSymSG, kSymWarps, kSymSrc>,
+                                                      kSymWarps * 32, sym_smem_bytes<2>(kSymWarps));
+        return std::max(v, 1);
+    }();
+    static const int occ3 = [] {
+        int v = 0;
+        cudaFuncSetAttribute(k_repulse_sym<3, false, kSymSG, kSymWarps, kSymSrc>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, sym_smem_bytes<3>(kSymWarps));
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_repulse_sym<3, false, kSymSG, kSymWarps, kSymSrc>,
+                                                      kSymWarps * 32, sym_smem_bytes<3>(kSymWarps));
+        return std::max(v, 1);
+    }();
+    const int o = dim == 3 ? occ3 : occ2;
     p.full_grid = (int64_t)sm_count() * o;
     t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>(p.full_grid, t.U));
     int32_t ms = 1;
@@ -773,12 +771,11 @@ EntropyPlan plan_entropy(int32_t n) {
     t.Ub = (int32_t)((n + kBlock - 1) / kBlock);
     t.c = TPB / kBlock;
     t.U = tri_prefix(t.TB, t);
-    static int occ = 0;
-    if (!occ) {
+    static const int occ = [] {
         int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_entropy_tri<2, false>, kBlock, 0);
-        occ = std::max(o, 1);
-    }
+        return std::max(o, 1);
+    }();
     t.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * occ, t.U));
     p.nblocks = t.G;
     return p;
