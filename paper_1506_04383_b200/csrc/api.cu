@@ -926,7 +926,7 @@ bool graphs_enabled() {
 // captured launches depend on (pointers, sizes, parameters).  A hit relaunches
 // the executable graph; capture + instantiate is paid once per distinct key.
 struct GraphKey {
-    const void* p[16];
+    const void* p[17];
     int64_t v[8];
     float f[2];
     bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
@@ -948,8 +948,8 @@ GraphKey make_key(const mm_sset* S, int dim, float alpha, float q, const mm_appr
     GraphKey k;
     memset(&k, 0, sizeof(k));
     (void)st;  // an executable graph may be launched into any stream
-    const void* ps[16] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
-                          sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child};
+    const void* ps[17] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
+                          sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child, sb.jpart};
     memcpy(k.p, ps, sizeof(ps));
     k.v[0] = S->n;
     k.v[1] = S->nnz;
