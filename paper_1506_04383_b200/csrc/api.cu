@@ -315,7 +315,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     RepulsePlan p;
     SymPlan sp;
     if (ap) {
-        e = launch_centroid(dim, ap->k, sb.mptr, sb.mem, x_in, sb.rep_hi, sb.rep_lo, st);
+        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rep_hi, sb.rep_lo, st);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
         e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, ap->ancestor, p, sb.part, st);

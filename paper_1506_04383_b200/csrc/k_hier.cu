@@ -212,21 +212,35 @@ __global__ void k_compose(int32_t n, const int32_t* __restrict__ a, const int32_
 }
 
 // Representative x'_v' = unweighted mean of the members (Q11),
-// accumulated in FP64 in ascending member order and stored as hi + lo floats
-// (hi = fl32(mean), lo = fl32(mean - hi)); rep_hi.w = nu(v') (Q10).
-template <int DIM>
+// accumulated in FP64 and stored as hi + lo floats (hi = fl32(mean),
+// lo = fl32(mean - hi)); rep_hi.w = nu(v') (Q10).  G lanes per
+// representative (G from the mean cluster size: 2 at h = 2, 32 at h = 7):
+// lane l sums members l, l+G, ... in order, then a fixed shuffle tree.
+template <int DIM, int G>
 __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
                            const float* __restrict__ x, float4* __restrict__ rep_hi, float4* __restrict__ rep_lo) {
-    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v >= k) return;
-    const int32_t b = mptr[v], e = mptr[v + 1];
+    const int64_t tg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int32_t v = (int32_t)(tg / G);
+    const int lg = (int)(tg & (G - 1));
     double sx = 0.0, sy = 0.0, sz = 0.0;
-    for (int32_t t = b; t < e; ++t) {
-        const float4 p = load_x<DIM>(x, mem[t]);
-        sx += p.x;
-        sy += p.y;
-        sz += p.z;
+    int32_t b = 0, e = 0;
+    if (v < k) {
+        b = mptr[v];
+        e = mptr[v + 1];
+        for (int32_t t = b + lg; t < e; t += G) {
+            const float4 p = load_x<DIM>(x, __ldg(mem + t));
+            sx += p.x;
+            sy += p.y;
+            sz += p.z;
+        }
     }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        sx += __shfl_xor_sync(0xffffffffu, sx, o, G);
+        sy += __shfl_xor_sync(0xffffffffu, sy, o, G);
+        if constexpr (DIM == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o, G);
+    }
+    if (v >= k || lg != 0) return;
     const double nu = (double)(e - b);
     const double mx = sx / nu, my = sy / nu, mz = DIM == 3 ? sz / nu : 0.0;
     const float hx = (float)mx, hy = (float)my, hz = (float)mz;
@@ -497,11 +511,25 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
     return cudaGetLastError();
 }
 
-cudaError_t launch_centroid(int dim, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
+cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
                             float4* rep_hi, float4* rep_lo, cudaStream_t st) {
     LaunchScope ls("centroid", st);
-    if (dim == 2) k_centroid<2><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo);
-    else k_centroid<3><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo);
+    // lanes per representative: about 4 members per lane
+    const double mean = k > 0 ? (double)n / k : 1.0;
+    int G = 1;
+    while (G < 32 && 4.0 * (2 * G) <= mean) G *= 2;
+    const int nb = nblk((int64_t)k * G);
+#define MM_C(D)                                                                               \
+    switch (G) {                                                                              \
+        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
+        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
+        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
+        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
+        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break; \
+        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break; \
+    }
+    if (dim == 2) { MM_C(2) } else { MM_C(3) }
+#undef MM_C
     return cudaGetLastError();
 }
 

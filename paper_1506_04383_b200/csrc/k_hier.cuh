@@ -28,7 +28,7 @@ cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr,
                          int32_t* key_sorted, int32_t* iota, int32_t* cnt, void* tmp, size_t tmp_bytes,
                          cudaStream_t st);
 cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int32_t* out, cudaStream_t st);
-cudaError_t launch_centroid(int dim, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
+cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
                             float4* rep_hi, float4* rep_lo, cudaStream_t st);
 cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
                            int32_t level, float* x, cudaStream_t st);
