@@ -307,7 +307,8 @@ cudaError_t prepare_approx(int32_t n, const mm_approx* ap, SweepBufs& sb, cudaSt
 
 // One sweep with all buffers prepared (graph-capturable: no allocation, no sync).
 cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* x_in,
-                       float* x_out, mm_sweep_stats* stats, const SweepBufs& sb, cudaStream_t st) {
+                       float* x_out, mm_sweep_stats* stats, const SweepBufs& sb, cudaStream_t st,
+                       const double* alpha_dev = nullptr) {
     const int32_t n = S->n;
     const double mean_row = (double)S->nnz / (double)n;
     const bool qpow = q != 0.0f;
@@ -335,6 +336,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     ga.w = S->w;
     ga.x = x_in;
     ga.alpha = alpha;
+    ga.alpha_dev = alpha_dev;
     ga.q = q;
     ga.part = sb.part;
     ga.sch = p.sch;
@@ -1069,11 +1071,175 @@ struct FixedRunner : Runner {
 // <- max(factor alpha, alpha_min); at alpha_min until converged (or the cap).
 // Each decision needs the relative change of the sweep just run: the fused
 // stats are read back after every sweep (one small D2H + sync per sweep).
+// ------------------------------------------------------------------ device-driven schedule loop
+// The schedule of one level as ONE CUDA graph: a conditional WHILE
+// node whose body runs a sweep, a one-thread decision kernel that applies the
+// schedule's rules to the sweep's fused statistics in device memory, and a
+// conditional IF node holding the second (ping-pong) sweep and decision.  The
+// decisions are the host runner's, in the same double arithmetic, so the
+// sweep count and every alpha are identical; the host waits once per level
+// instead of once per sweep.
+struct SchedDev {
+    double alpha;
+    int32_t it, max_it, fin, done, err, count, cur, pad;
+};
+
+__global__ void k_sched_init(SchedDev* s, double alpha, double alpha_min, int32_t a, int32_t max_final) {
+    s->alpha = alpha;
+    s->it = 0;
+    s->fin = alpha <= alpha_min;
+    s->max_it = s->fin ? max_final : a;
+    s->done = 0;
+    s->err = 0;
+    s->count = 0;
+    s->cur = 0;
+}
+
+__global__ void k_sched_decide(SchedDev* s, const mm_sweep_stats* st, double alpha_min, double factor, double eps,
+                               int32_t a, int32_t max_final, cudaGraphConditionalHandle h_while,
+                               cudaGraphConditionalHandle h_if, int set_if) {
+    if (!s->done) {
+        s->count += 1;
+        s->cur ^= 1;
+        if (st->flags & 1) {
+            s->err = 1;
+            s->done = 1;
+        } else {
+            const double rel = st->x2 > 0 ? sqrt(st->dx2) / sqrt(st->x2) : INFINITY;
+            s->it += 1;
+            if (rel < eps || s->it >= s->max_it) {  // round over (converged or a sweeps done)
+                if (s->fin) {
+                    s->done = 1;
+                } else {
+                    s->alpha = fmax(s->alpha * factor, alpha_min);
+                    s->it = 0;
+                    s->fin = s->alpha <= alpha_min;
+                    s->max_it = s->fin ? max_final : a;
+                }
+            }
+        }
+    }
+    const unsigned go = s->done ? 0u : 1u;
+    cudaGraphSetConditional(h_while, go);
+    if (set_if) cudaGraphSetConditional(h_if, go);
+}
+
 struct ScheduleRunner : Runner {
     mm_schedule sch;
+    mm_status run_graph(const mm_sset* S, int dim, float q, const mm_approx* ap, const float* src, float* A,
+                        float* B, mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, bool start_at_min,
+                        const float** res, int32_t* nsw) {
+        const int st_w = stride_of(dim);
+        const size_t xbytes = (size_t)S->n * st_w * sizeof(float);
+        DevBuf state(sizeof(SchedDev), ls);
+        if (!state.p) { set_err("mm_layout_schedule: out of device memory"); return MM_ERR_OUT_OF_MEMORY; }
+        SchedDev* sd = (SchedDev*)state.p;
+        const double alpha0 = start_at_min ? sch.alpha_min : sch.alpha0;
+        k_sched_init<<<1, 1, 0, ls>>>(sd, alpha0, sch.alpha_min, sch.a, sch.max_final_iters);
+        MM_CU(cudaGetLastError(), "mm_layout_schedule init");
+        // ping-pong P -> Q -> P ...; a src outside {A, B} is copied into B first
+        float* P;
+        float* Q;
+        if (src == A) {
+            P = A;
+            Q = B;
+        } else {
+            if (src != B) MM_CU(cudaMemcpyAsync(B, src, xbytes, cudaMemcpyDeviceToDevice, ls), "mm_layout_schedule copy");
+            P = B;
+            Q = A;
+        }
+        const double* ad = &sd->alpha;
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaError_t e = cudaGraphCreate(&g, 0);
+        cudaGraphConditionalHandle hw = 0, hi = 0;
+        cudaGraphNodeParams wp = {};
+        cudaGraphNode_t wn = nullptr;
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hw, g, 1, cudaGraphCondAssignDefault);
+        if (e == cudaSuccess) {
+            wp.type = cudaGraphNodeTypeConditional;
+            wp.conditional.handle = hw;
+            wp.conditional.type = cudaGraphCondTypeWhile;
+            wp.conditional.size = 1;
+            e = cudaGraphAddNode(&wn, g, nullptr, 0, &wp);
+        }
+        cudaGraph_t body = e == cudaSuccess ? wp.conditional.phGraph_out[0] : nullptr;
+        if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&hi, body, 0, cudaGraphCondAssignDefault);
+        const double amin = sch.alpha_min, fac = sch.factor, eps = sch.eps;
+        const int32_t a = sch.a, mf = sch.max_final_iters;
+        cudaGraph_t cap = nullptr;
+        if (e == cudaSuccess)
+            e = cudaStreamBeginCaptureToGraph(ls, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+        if (e == cudaSuccess) {
+            cudaError_t ec = sweep_core(S, dim, (float)alpha0, q, ap, P, Q, dstats, sb, ls, ad);
+            if (ec == cudaSuccess) {
+                k_sched_decide<<<1, 1, 0, ls>>>(sd, dstats, amin, fac, eps, a, mf, hw, hi, 1);
+                ec = cudaGetLastError();
+            }
+            // the IF node after the first decision, spliced into the capture
+            cudaGraphNodeParams ip = {};
+            cudaGraphNode_t in = nullptr;
+            if (ec == cudaSuccess) {
+                cudaStreamCaptureStatus cs;
+                cudaGraph_t cg = nullptr;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t nd = 0;
+                ec = cudaStreamGetCaptureInfo(ls, &cs, nullptr, &cg, &deps, &nd);
+                if (ec == cudaSuccess) {
+                    ip.type = cudaGraphNodeTypeConditional;
+                    ip.conditional.handle = hi;
+                    ip.conditional.type = cudaGraphCondTypeIf;
+                    ip.conditional.size = 1;
+                    ec = cudaGraphAddNode(&in, cg, deps, nd, &ip);
+                }
+                if (ec == cudaSuccess) ec = cudaStreamUpdateCaptureDependencies(ls, &in, 1, cudaStreamSetCaptureDependencies);
+            }
+            e = cudaStreamEndCapture(ls, &cap);
+            if (ec != cudaSuccess) e = ec;
+            if (e == cudaSuccess) {
+                e = cudaStreamBeginCaptureToGraph(ls, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                  cudaStreamCaptureModeThreadLocal);
+                if (e == cudaSuccess) {
+                    ec = sweep_core(S, dim, (float)alpha0, q, ap, Q, P, dstats, sb, ls, ad);
+                    if (ec == cudaSuccess) {
+                        k_sched_decide<<<1, 1, 0, ls>>>(sd, dstats, amin, fac, eps, a, mf, hw, hi, 0);
+                        ec = cudaGetLastError();
+                    }
+                    e = cudaStreamEndCapture(ls, &cap);
+                    if (ec != cudaSuccess) e = ec;
+                }
+            }
+        }
+        if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
+        if (e == cudaSuccess) e = cudaGraphLaunch(exec, ls);
+        SchedDev h{};
+        if (e == cudaSuccess) e = cudaMemcpyAsync(&h, sd, sizeof(h), cudaMemcpyDeviceToHost, ls);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
+        if (exec) cudaGraphExecDestroy(exec);
+        if (g) cudaGraphDestroy(g);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            set_err("mm_layout_schedule: device-driven schedule graph: %s", cudaGetErrorString(e));
+            return MM_ERR_CUDA;
+        }
+        if (h.err) {
+            set_err("mm_layout_schedule: non-finite coordinate produced");
+            return MM_ERR_NONFINITE;
+        }
+        *res = (h.count & 1) ? Q : P;
+        *nsw = h.count;
+        return MM_OK;
+    }
     mm_status run(const mm_sset* S, int dim, float q, const mm_approx* ap, const float* src, float* A, float* B,
                   mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int32_t, bool start_at_min,
                   const float** res, int32_t* nsw) override {
+        // one graph per level, the host waiting once (MM_SCHED_GRAPH=0: host loop)
+        static const bool dev_loop = [] {
+            const char* e = getenv("MM_SCHED_GRAPH");
+            return !(e && e[0] == '0');
+        }();
+        if (dev_loop && graphs_enabled() && sch.a >= 1 && sch.max_final_iters >= 1)
+            return run_graph(S, dim, q, ap, src, A, B, dstats, sb, ls, start_at_min, res, nsw);
         double alpha = start_at_min ? sch.alpha_min : sch.alpha0;
         const float* cur = src;
         int32_t count = 0;

@@ -61,6 +61,7 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
 constexpr int kGatherUnroll = MM_GATHER_UNROLL;
 template <int DIM, bool QPOW, int G>
 __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a, float cexp) {
+    if (a.alpha_dev) a.alpha = (float)*a.alpha_dev;  // same rounding as the host path's (float)alpha
     const int lg = threadIdx.x & (G - 1);
     constexpr int VPB = kGBlock / G;  // vertices per block iteration
     double v_dx2 = 0.0, v_x2 = 0.0, v_st = 0.0;

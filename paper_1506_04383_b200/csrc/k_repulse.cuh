@@ -72,6 +72,7 @@ struct GatherArgs {
     const float* x;
     float alpha;
     float q;
+    const double* alpha_dev = nullptr;  // non-NULL: alpha read from device memory (device-driven schedule)
     const float* part;   // [slots][n] stride 2 (dim 2) or 4 (dim 3)
     Sched sch;           // schedule that produced `part` (slot count per target block)
     int tpb;             // targets per block of that schedule
