@@ -931,6 +931,9 @@ struct GraphKey {
     const void* p[17];
     int64_t v[8];
     float f[2];
+    int32_t kind = 0;      // 0: K fixed sweeps; 1: device-driven schedule loop of one level
+    int32_t si[3] = {0, 0, 0};
+    double sd[4] = {0, 0, 0, 0};
     bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
 };
 struct GraphEntry {
@@ -943,6 +946,33 @@ std::mutex g_graph_mu;
 std::vector<GraphEntry> g_graphs;
 uint64_t g_graph_clock = 0;
 constexpr size_t kGraphCacheMax = 16;
+
+// cache lookup: on a hit the launch counter advances by the graph's kernels
+// (for a schedule graph: one body pass per lookup, an undercount)
+cudaGraphExec_t graph_cache_find(const GraphKey& key) {
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    for (auto& e : g_graphs) {
+        if (e.key == key) {
+            e.stamp = ++g_graph_clock;
+            g_launches.fetch_add(e.kernels, std::memory_order_relaxed);
+            return e.exec;
+        }
+    }
+    return nullptr;
+}
+
+void graph_cache_insert(const GraphKey& key, cudaGraphExec_t exec, int64_t kernels) {
+    std::lock_guard<std::mutex> g(g_graph_mu);
+    if (g_graphs.size() >= kGraphCacheMax) {
+        size_t victim = 0;
+        for (size_t i = 1; i < g_graphs.size(); ++i)
+            if (g_graphs[i].stamp < g_graphs[victim].stamp) victim = i;
+        cudaDeviceSynchronize();  // the victim may still be running
+        cudaGraphExecDestroy(g_graphs[victim].exec);
+        g_graphs.erase(g_graphs.begin() + victim);
+    }
+    g_graphs.push_back(GraphEntry{key, exec, kernels, ++g_graph_clock});
+}
 
 GraphKey make_key(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap, const float* src,
                   const float* bufA, const float* bufB, int32_t K, const mm_sweep_stats* stats, const SweepBufs& sb,
@@ -992,16 +1022,7 @@ cudaError_t run_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm
         return cudaSuccess;
     }
     const GraphKey key = make_key(S, dim, alpha, q, ap, src, bufA, bufB, K, stats, sb, st);
-    {
-        std::lock_guard<std::mutex> g(g_graph_mu);
-        for (auto& e : g_graphs) {
-            if (e.key == key) {
-                e.stamp = ++g_graph_clock;
-                g_launches.fetch_add(e.kernels, std::memory_order_relaxed);
-                return cudaGraphLaunch(e.exec, st);
-            }
-        }
-    }
+    if (cudaGraphExec_t hit = graph_cache_find(key)) return cudaGraphLaunch(hit, st);
     const int64_t l0 = g_launches.load();
     cudaError_t err = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
     if (err != cudaSuccess) return err;
@@ -1022,16 +1043,7 @@ cudaError_t run_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm
         return err;
     }
     err = cudaGraphLaunch(exec, st);
-    std::lock_guard<std::mutex> g(g_graph_mu);
-    if (g_graphs.size() >= kGraphCacheMax) {
-        size_t victim = 0;
-        for (size_t i = 1; i < g_graphs.size(); ++i)
-            if (g_graphs[i].stamp < g_graphs[victim].stamp) victim = i;
-        cudaDeviceSynchronize();  // the victim may still be running
-        cudaGraphExecDestroy(g_graphs[victim].exec);
-        g_graphs.erase(g_graphs.begin() + victim);
-    }
-    g_graphs.push_back(GraphEntry{key, exec, g_launches.load() - l0, ++g_graph_clock});
+    graph_cache_insert(key, exec, g_launches.load() - l0);
     return err;
 }
 
@@ -1083,6 +1095,7 @@ struct SchedDev {
     double alpha;
     int32_t it, max_it, fin, done, err, count, cur, pad;
 };
+__device__ SchedDev g_sched_state;
 
 __global__ void k_sched_init(SchedDev* s, double alpha, double alpha_min, int32_t a, int32_t max_final) {
     s->alpha = alpha;
@@ -1131,11 +1144,15 @@ struct ScheduleRunner : Runner {
                         const float** res, int32_t* nsw) {
         const int st_w = stride_of(dim);
         const size_t xbytes = (size_t)S->n * st_w * sizeof(float);
-        DevBuf state(sizeof(SchedDev), ls);
-        if (!state.p) { set_err("mm_layout_schedule: out of device memory"); return MM_ERR_OUT_OF_MEMORY; }
-        SchedDev* sd = (SchedDev*)state.p;
+        // the loop state lives in a fixed device symbol (layouts are serialised
+        // by the driver's stream lock), so the graph can be cached and relaunched
+        SchedDev* sd = nullptr;
+        MM_CU(cudaGetSymbolAddress((void**)&sd, g_sched_state), "mm_layout_schedule state");
         const double alpha0 = start_at_min ? sch.alpha_min : sch.alpha0;
-        k_sched_init<<<1, 1, 0, ls>>>(sd, alpha0, sch.alpha_min, sch.a, sch.max_final_iters);
+        {
+            LaunchScope lsc("sched_init", ls);
+            k_sched_init<<<1, 1, 0, ls>>>(sd, alpha0, sch.alpha_min, sch.a, sch.max_final_iters);
+        }
         MM_CU(cudaGetLastError(), "mm_layout_schedule init");
         // ping-pong P -> Q -> P ...; a src outside {A, B} is copied into B first
         float* P;
@@ -1149,6 +1166,29 @@ struct ScheduleRunner : Runner {
             Q = A;
         }
         const double* ad = &sd->alpha;
+        GraphKey key = make_key(S, dim, (float)alpha0, q, ap, P, A, B, 0, dstats, sb, ls);
+        key.kind = 1;
+        key.si[0] = sch.a;
+        key.si[1] = sch.max_final_iters;
+        key.sd[0] = sch.alpha_min;
+        key.sd[1] = sch.factor;
+        key.sd[2] = sch.eps;
+        const int64_t c0 = g_launches.load();
+        cudaGraphExec_t cached = graph_cache_find(key);  // adds one sweep's kernels (k_half)
+        SchedDev h{};
+        if (cached) {
+            const int64_t k_half = g_launches.load() - c0;
+            cudaError_t e = cudaGraphLaunch(cached, ls);
+            if (e == cudaSuccess) e = cudaMemcpyAsync(&h, sd, sizeof(h), cudaMemcpyDeviceToHost, ls);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
+            if (e != cudaSuccess) {
+                set_err("mm_layout_schedule: schedule graph launch: %s", cudaGetErrorString(e));
+                return MM_ERR_CUDA;
+            }
+            g_launches.fetch_add((int64_t)h.count * k_half - k_half, std::memory_order_relaxed);
+            return finish(h, P, Q, res, nsw);
+        }
+        const int64_t l0 = g_launches.load();
         cudaGraph_t g = nullptr;
         cudaGraphExec_t exec = nullptr;
         cudaError_t e = cudaGraphCreate(&g, 0);
@@ -1173,6 +1213,7 @@ struct ScheduleRunner : Runner {
         if (e == cudaSuccess) {
             cudaError_t ec = sweep_core(S, dim, (float)alpha0, q, ap, P, Q, dstats, sb, ls, ad);
             if (ec == cudaSuccess) {
+                LaunchScope lsc("sched_decide", ls);
                 k_sched_decide<<<1, 1, 0, ls>>>(sd, dstats, amin, fac, eps, a, mf, hw, hi, 1);
                 ec = cudaGetLastError();
             }
@@ -1202,6 +1243,7 @@ struct ScheduleRunner : Runner {
                 if (e == cudaSuccess) {
                     ec = sweep_core(S, dim, (float)alpha0, q, ap, Q, P, dstats, sb, ls, ad);
                     if (ec == cudaSuccess) {
+                        LaunchScope lsc("sched_decide", ls);
                         k_sched_decide<<<1, 1, 0, ls>>>(sd, dstats, amin, fac, eps, a, mf, hw, hi, 0);
                         ec = cudaGetLastError();
                     }
@@ -1211,17 +1253,23 @@ struct ScheduleRunner : Runner {
             }
         }
         if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, g, 0);
+        if (g) cudaGraphDestroy(g);
+        // kernels per sweep (+ its decision): the capture counted both halves once
+        const int64_t k_half = (g_launches.load() - l0) / 2;
         if (e == cudaSuccess) e = cudaGraphLaunch(exec, ls);
-        SchedDev h{};
         if (e == cudaSuccess) e = cudaMemcpyAsync(&h, sd, sizeof(h), cudaMemcpyDeviceToHost, ls);
         if (e == cudaSuccess) e = cudaStreamSynchronize(ls);
-        if (exec) cudaGraphExecDestroy(exec);
-        if (g) cudaGraphDestroy(g);
         if (e != cudaSuccess) {
+            if (exec) cudaGraphExecDestroy(exec);
             cudaGetLastError();
             set_err("mm_layout_schedule: device-driven schedule graph: %s", cudaGetErrorString(e));
             return MM_ERR_CUDA;
         }
+        graph_cache_insert(key, exec, k_half);
+        g_launches.fetch_add((int64_t)h.count * k_half - 2 * k_half, std::memory_order_relaxed);
+        return finish(h, P, Q, res, nsw);
+    }
+    static mm_status finish(const SchedDev& h, float* P, float* Q, const float** res, int32_t* nsw) {
         if (h.err) {
             set_err("mm_layout_schedule: non-finite coordinate produced");
             return MM_ERR_NONFINITE;
