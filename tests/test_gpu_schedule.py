@@ -103,3 +103,23 @@ def test_schedule_sclap_disc(mm, name, dim):
                                       disc=True)[1][2]
 
     assert_energy_or_chaos(rep["energy"], eo[2], control, f"{name} sclap+disc")
+
+
+def test_device_loop_matches_host_loop(tmp_path):
+    """The device-driven schedule (one conditional-node CUDA graph per level)
+    makes the host loop's decisions on the device: identical sweep counts and
+    bit-identical layouts (same kernels, same order, same alpha values)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for mode in ("1", "0"):
+        out = tmp_path / f"mode{mode}.npz"
+        r = subprocess.run([sys.executable, "-m", "tests.sched_mode_case", str(out)], cwd=root,
+                           env=dict(os.environ, MM_SCHED_GRAPH=mode), capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[mode] = np.load(out)
+    for k in outs["1"].files:
+        assert np.array_equal(outs["1"][k], outs["0"][k]), k
