@@ -238,10 +238,21 @@ def _dim_of(xt) -> int:
 
 
 # ------------------------------------------------------------------ API
+def sweep_workspace(n: int, dim: int, k: int = 0) -> int:
+    """Scratch bytes mm_sweep needs (k > 0: Eq.(3) with k representatives)."""
+    b = ctypes.c_size_t(0)
+    ap = mm_approx(int(k), None, None) if k > 0 else None
+    _check(load().mm_sweep_workspace(int(n), int(dim), ctypes.byref(ap) if ap else None, ctypes.byref(b)),
+           "mm_sweep_workspace")
+    return int(b.value)
+
+
 def sweep(S: DeviceSSet, x, alpha: float, q: float, parent=None, ancestor=None, k: int = 0,
-          out=None, stats: bool = False):
+          out=None, stats: bool = False, workspace=None):
     """One Jacobi sweep (Eq.(2), or Eq.(3) when parent/ancestor/k are given).
-    x: CUDA float32 tensor (n,2) or (n,4).  Returns x_out (and the stats dict)."""
+    x: CUDA float32 tensor (n,2) or (n,4).  workspace: optional CUDA uint8 tensor
+    of at least sweep_workspace() bytes (else the library allocates).
+    Returns x_out (and the stats dict)."""
     torch = _torch()
     L = load()
     dim = _dim_of(x)
@@ -254,8 +265,9 @@ def sweep(S: DeviceSSet, x, alpha: float, q: float, parent=None, ancestor=None, 
     if parent is not None:
         ap = mm_approx(int(k), _ptr(parent), _ptr(ancestor))
     s = S.c_struct()
+    ws, wsb = (None, 0) if workspace is None else (_ptr(workspace), workspace.numel() * workspace.element_size())
     rc = L.mm_sweep(ctypes.byref(s), dim, float(alpha), float(q), ctypes.byref(ap) if ap else None,
-                    _ptr(x), _ptr(out), _ptr(st), None, 0, _stream_ptr(x.device))
+                    _ptr(x), _ptr(out), _ptr(st), ws, wsb, _stream_ptr(x.device))
     _check(rc, "mm_sweep")
     if stats:
         h = st.cpu().numpy()

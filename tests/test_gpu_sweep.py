@@ -272,3 +272,29 @@ def test_empty_and_degenerate_inputs_rejected(mm):
     par = torch.zeros(w.n, dtype=torch.int32, device="cuda")
     with pytest.raises(mm.MMError):
         mm.sweep(Sd, xd, 0.1, 0.0, parent=par, ancestor=par, k=w.n + 1)
+
+
+@pytest.mark.parametrize("name,approx", [("cfg2", False), ("cfg3_mesh64", True)])
+def test_caller_workspace_bitwise(mm, name, approx):
+    """mm_sweep with caller-provided scratch (mm_sweep_workspace bytes) equals the
+    library-allocated path bit for bit (exact: the symmetric kernel at cfg2)."""
+    import torch
+
+    w = workload(name)
+    x = w.x0 if w.x0 is not None else configs.random_state(w.n, w.dim, seed=2, scale=64.0)
+    S = mm.sset_to_device(w.S)
+    xd = mm.coords_to_device(x)
+    kw, k = {}, 0
+    if approx:
+        lv = oracle_hierarchy(name)
+        anc = oracle.ancestor(lv, 0, 2)
+        k = lv[2].n
+        kw = dict(parent=torch.from_numpy(lv[0].parent.astype(np.int32)).cuda(),
+                  ancestor=torch.from_numpy(anc.astype(np.int32)).cuda(), k=k)
+    a = mm.sweep(S, xd, w.alpha, w.q, **kw)
+    ws = torch.empty(mm.sweep_workspace(w.n, w.dim, k), dtype=torch.uint8, device="cuda")
+    b = mm.sweep(S, xd, w.alpha, w.q, workspace=ws, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    with pytest.raises(mm.MMError):
+        mm.sweep(S, xd, w.alpha, w.q, workspace=ws[:64], **kw)
