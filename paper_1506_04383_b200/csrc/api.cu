@@ -18,6 +18,7 @@
 
 #include "k_fullstress.cuh"
 #include "k_hier.cuh"
+#include "k_small.cuh"
 #include "k_sclap.cuh"
 #include "k_repulse.cuh"
 
@@ -254,6 +255,12 @@ int part_slots(int32_t n, int dim, int32_t n_src, bool approx) {
     return slots;
 }
 
+// per-CTA FP64 partials: the gather's [blocks][3] (bound: G = 32) or the
+// small-level kernel's [2][grid][4], whichever is larger
+size_t stat_partial_doubles(int32_t n) {
+    return std::max((size_t)gather_blocks(n, 1e9) * 3, (size_t)small_level_partials(n) * 4);
+}
+
 size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) {
     const int32_t n_src = approx ? k : n;
     const int slots = part_slots(n, dim, n_src, approx);
@@ -261,7 +268,7 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
     if (!approx && use_sym(n, dim))
         b += al((size_t)sym_jpart_rows(plan_repulse_sym(n, dim)) * n * stride_of(dim) * sizeof(float));
     (void)mean_row;
-    b += al((size_t)gather_blocks(n, 1e9) * 3 * sizeof(double));  // bound: G = 32
+    b += al(stat_partial_doubles(n) * sizeof(double));
     b += al(sizeof(int32_t) * 4);
     if (approx) {
         b += 2 * al((size_t)k * sizeof(float4)) + al((size_t)(k + 1) * 4) + al((size_t)n * 4);
@@ -278,7 +285,7 @@ bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double 
     if (!approx && use_sym(n, dim))
         sb.jpart = cv.take<float>((size_t)sym_jpart_rows(plan_repulse_sym(n, dim)) * n * stride_of(dim));
     (void)mean_row;
-    sb.stat_partial = cv.take<double>((size_t)gather_blocks(n, 1e9) * 3);
+    sb.stat_partial = cv.take<double>(stat_partial_doubles(n));
     sb.flags = cv.take<int32_t>(4);
     if (approx) {
         sb.rep_hi = cv.take<float4>(k);
@@ -1062,8 +1069,76 @@ struct Runner {
                           bool start_at_min, const float** res, int32_t* sweeps) = 0;
 };
 
+// Small levels: all sweeps of the level in one persistent cooperative kernel
+// (k_small.cu).  mode 0: K sweeps at alpha0 (no host wait; the result buffer
+// follows from K's parity); mode 1: the schedule, decided on the device (one
+// host wait for the sweep count).
+mm_status run_small(const mm_sset* S, int dim, float q, const mm_approx* ap, const float* src, float* A, float* B,
+                    mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int mode, int32_t K, double alpha0,
+                    const mm_schedule* sch, const float** res, int32_t* nsw) {
+    const size_t xbytes = (size_t)S->n * stride_of(dim) * sizeof(float);
+    float *x0, *x1;
+    if (src == A) {
+        x0 = A;
+        x1 = B;
+    } else {
+        if (src != B) MM_CU(cudaMemcpyAsync(B, src, xbytes, cudaMemcpyDeviceToDevice, ls), "small level copy");
+        x0 = B;
+        x1 = A;
+    }
+    SmallArgs a;
+    a.n = S->n;
+    a.k = ap ? ap->k : 0;
+    a.rp = S->row_ptr;
+    a.col = S->col;
+    a.d = S->d;
+    a.w = S->w;
+    a.x0 = x0;
+    a.x1 = x1;
+    a.q = q;
+    if (ap) {
+        a.anc = ap->ancestor;
+        a.parent = ap->parent;
+        a.mptr = sb.mptr;
+        a.mem = sb.mem;
+        a.cptr = sb.cptr;
+        a.child = sb.child;
+        a.rep_hi = sb.rep_hi;
+        a.rep_lo = sb.rep_lo;
+    }
+    a.mode = mode;
+    a.K = K;
+    a.alpha0 = alpha0;
+    if (sch) {
+        a.alpha_min = sch->alpha_min;
+        a.factor = sch->factor;
+        a.eps = sch->eps;
+        a.rounds = sch->a;
+        a.max_final = sch->max_final_iters;
+    }
+    a.partial = sb.stat_partial;
+    a.result = sb.flags;  // re-armed (memset) before the next level's sweeps
+    a.stats = dstats;
+    MM_CU(launch_small_level(dim, ap != nullptr, a, ls), "small level");
+    if (mode == 0) {
+        *res = (K & 1) ? x1 : x0;
+        *nsw = K;
+        return MM_OK;
+    }
+    int32_t h[3] = {0, 0, 0};
+    MM_CU(cudaMemcpyAsync(h, sb.flags, sizeof(h), cudaMemcpyDeviceToHost, ls), "small level d2h");
+    MM_CU(cudaStreamSynchronize(ls), "small level sync");
+    if (h[1]) {
+        set_err("mm_layout_schedule: non-finite coordinate produced");
+        return MM_ERR_NONFINITE;
+    }
+    *res = h[2] ? x1 : x0;
+    *nsw = h[0];
+    return MM_OK;
+}
+
 // Fixed alpha and sweep counts (BASELINE.json configs): the K sweeps of a
-// level are one cached CUDA graph.
+// level are one cached CUDA graph (or, for a small level, one persistent kernel).
 struct FixedRunner : Runner {
     float alpha;
     const int32_t* sweeps;
@@ -1072,6 +1147,8 @@ struct FixedRunner : Runner {
                   mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int32_t level, bool,
                   const float** res, int32_t* nsw) override {
         const int32_t K = sweeps[std::min(level, nsweeps - 1)];
+        if (K >= 1 && small_level_ok(dim, S->n, ap ? ap->k : 0, ap != nullptr))
+            return run_small(S, dim, q, ap, src, A, B, dstats, sb, ls, 0, K, alpha, nullptr, res, nsw);
         MM_CU(run_sweeps(S, dim, alpha, q, ap, src, A, B, K, dstats, sb, ls, res), "mm_layout sweeps");
         *nsw = K;
         return MM_OK;
@@ -1286,6 +1363,9 @@ struct ScheduleRunner : Runner {
             const char* e = getenv("MM_SCHED_GRAPH");
             return !(e && e[0] == '0');
         }();
+        if (sch.a >= 1 && sch.max_final_iters >= 1 && small_level_ok(dim, S->n, ap ? ap->k : 0, ap != nullptr))
+            return run_small(S, dim, q, ap, src, A, B, dstats, sb, ls, 1, 0,
+                             start_at_min ? sch.alpha_min : sch.alpha0, &sch, res, nsw);
         if (dev_loop && graphs_enabled() && sch.a >= 1 && sch.max_final_iters >= 1)
             return run_graph(S, dim, q, ap, src, A, B, dstats, sb, ls, start_at_min, res, nsw);
         double alpha = start_at_min ? sch.alpha_min : sch.alpha0;
@@ -1491,6 +1571,12 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
             if ((s = run.run(&Sl, dim, q, app, cur, other, (float*)cur, dstats, sbl, ls, l, dynamic, &res, &nsw)) !=
                 MM_OK)
                 return s;
+            if (trace_on()) {
+                char msg[160];
+                snprintf(msg, sizeof(msg), "layout: level %d done (n %d, k %d, %d sweeps enqueued)", l, nf,
+                         app ? ap.k : 0, nsw);
+                trace(msg);
+            }
             cur = res;
             R.n_level[l] = nf;
             R.k_level[l] = app ? ap.k : 0;
