@@ -91,12 +91,13 @@ __device__ __forceinline__ void pair_term(const float4& xi, float sx, float sy, 
     if constexpr (DIM == 3) acc.z = fmaf(dz, inv, acc.z);
 }
 
-template <int DIM, bool APPROX>
+template <int DIM, bool APPROX, int G>
 __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
     extern __shared__ float4 sm[];  // APPROX: [k] hi, [k] lo ; exact: [n] coordinates
     __shared__ double red[4][kSmallBlock / 32];
-    const unsigned G = gridDim.x;
+    const unsigned NB = gridDim.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int lg = tid & (G - 1);  // lane within the target's group of G lanes
     const float cexp = -(a.q + 2.0f) * 0.5f;
     const bool qpow = a.q != 0.0f;
     const float* xin = a.x0;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
     for (;;) {
         // ---- representatives of x_in (Eq.(3))
         if constexpr (APPROX) {
-            const int32_t gw = (int32_t)(blockIdx.x * (kSmallBlock / 32) + warp), nw = (int32_t)(G * (kSmallBlock / 32));
+            const int32_t gw = (int32_t)(blockIdx.x * (kSmallBlock / 32) + warp), nw = (int32_t)(NB * (kSmallBlock / 32));
             for (int32_t v = gw; v < a.k; v += nw) {
                 const int32_t b = __ldg(a.mptr + v), e = __ldg(a.mptr + v + 1);
                 double sx = 0.0, sy = 0.0, sz = 0.0;
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
                     a.rep_lo[v] = make_float4((float)(mx - hx), (float)(my - hy), (float)(mz - hz), 0.f);
                 }
             }
-            grid_barrier(G);
+            grid_barrier(NB);
             for (int32_t v = tid; v < a.k; v += kSmallBlock) {
                 sm[v] = __ldcg(a.rep_hi + v);
                 sm[a.k + v] = __ldcg(a.rep_lo + v);
@@ -148,17 +149,22 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
         double v_dx2 = 0.0, v_x2 = 0.0, v_st = 0.0;
         int32_t bad = 0;
         const float alpha_f = (float)alpha;
-        const int32_t gw = (int32_t)(blockIdx.x * (kSmallBlock / 32) + warp), nw = (int32_t)(G * (kSmallBlock / 32));
-        for (int32_t i = gw; i < a.n; i += nw) {
+        const int32_t gg = (int32_t)((blockIdx.x * kSmallBlock + tid) / G), ng = (int32_t)(NB * (kSmallBlock / G));
+        // all lanes of a warp run the same number of iterations (the shuffles need them)
+        const int32_t iters = (a.n + ng - 1) / ng;
+        for (int32_t r = 0; r < iters; ++r) {
+            const int32_t i0 = gg + r * ng;
+            const bool valid = i0 < a.n;
+            const int32_t i = valid ? i0 : a.n - 1;
             const float4 xi = load_xc<DIM>(xin, i);
             float4 R = make_float4(0.f, 0.f, 0.f, 0.f), C = R, A = R;
             if constexpr (APPROX) {
-                for (int32_t v = lane; v < a.k; v += 32) {
+                for (int32_t v = lg; v < a.k; v += G) {
                     const float4 h = sm[v], l = sm[a.k + v];
                     const float4 d4 = make_float4((xi.x - h.x) - l.x, (xi.y - h.y) - l.y, (xi.z - h.z) - l.z, 0.f);
                     pair_term<DIM>(d4, 0.f, 0.f, 0.f, h.w, cexp, qpow, R);
                 }
-                if (lane == 0) {  // own representative (Q25): into C, i.e. subtracted
+                if (lg == 0) {  // own representative (Q25): into C, i.e. subtracted
                     const int32_t hv = __ldg(a.anc + i);
                     const float4 h = sm[hv], l = sm[a.k + hv];
                     const float4 d4 = make_float4((xi.x - h.x) - l.x, (xi.y - h.y) - l.y, (xi.z - h.z) - l.z, 0.f);
@@ -166,14 +172,14 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
                 }
                 const int32_t p = __ldg(a.parent + i);
                 const int32_t c1 = __ldg(a.cptr + p + 1);
-                for (int32_t c = __ldg(a.cptr + p) + lane; c < c1; c += 32) {  // siblings under P(i)
+                for (int32_t c = __ldg(a.cptr + p) + lg; c < c1; c += G) {  // siblings under P(i)
                     const int32_t j = __ldg(a.child + c);
                     if (j == i) continue;
                     const float4 xj = load_xc<DIM>(xin, j);
                     pair_term<DIM>(xi, xj.x, xj.y, xj.z, 1.f, cexp, qpow, R);
                 }
             } else {
-                for (int32_t j = lane; j < a.n; j += 32) {
+                for (int32_t j = lg; j < a.n; j += G) {
                     const float4 sv = sm[j];
                     pair_term<DIM>(xi, sv.x, sv.y, sv.z, 1.f, cexp, qpow, R);  // j = i: dx = 0 -> 0
                 }
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
             // S_i: attraction, S-pair r-values (subtracted), stress
             float rho = 0.f, st = 0.f;
             const int64_t e0 = __ldg(a.rp + i), e1 = __ldg(a.rp + i + 1);
-            for (int64_t e = e0 + lane; e < e1; e += 32) {
+            for (int64_t e = e0 + lg; e < e1; e += G) {
                 const int32_t j = __ldg(a.col + e);
                 const float dd = __ldg(a.d + e), ww = __ldg(a.w + e);
                 const float4 xj = load_xc<DIM>(xin, j);
@@ -208,22 +214,22 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
                 st = fmaf(ww * dev, dev, st);
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                R.x += __shfl_xor_sync(0xffffffffu, R.x, o);
-                R.y += __shfl_xor_sync(0xffffffffu, R.y, o);
-                C.x += __shfl_xor_sync(0xffffffffu, C.x, o);
-                C.y += __shfl_xor_sync(0xffffffffu, C.y, o);
-                A.x += __shfl_xor_sync(0xffffffffu, A.x, o);
-                A.y += __shfl_xor_sync(0xffffffffu, A.y, o);
-                rho += __shfl_xor_sync(0xffffffffu, rho, o);
-                st += __shfl_xor_sync(0xffffffffu, st, o);
+            for (int o = G / 2; o > 0; o >>= 1) {
+                R.x += __shfl_xor_sync(0xffffffffu, R.x, o, G);
+                R.y += __shfl_xor_sync(0xffffffffu, R.y, o, G);
+                C.x += __shfl_xor_sync(0xffffffffu, C.x, o, G);
+                C.y += __shfl_xor_sync(0xffffffffu, C.y, o, G);
+                A.x += __shfl_xor_sync(0xffffffffu, A.x, o, G);
+                A.y += __shfl_xor_sync(0xffffffffu, A.y, o, G);
+                rho += __shfl_xor_sync(0xffffffffu, rho, o, G);
+                st += __shfl_xor_sync(0xffffffffu, st, o, G);
                 if constexpr (DIM == 3) {
-                    R.z += __shfl_xor_sync(0xffffffffu, R.z, o);
-                    C.z += __shfl_xor_sync(0xffffffffu, C.z, o);
-                    A.z += __shfl_xor_sync(0xffffffffu, A.z, o);
+                    R.z += __shfl_xor_sync(0xffffffffu, R.z, o, G);
+                    C.z += __shfl_xor_sync(0xffffffffu, C.z, o, G);
+                    A.z += __shfl_xor_sync(0xffffffffu, A.z, o, G);
                 }
             }
-            if (lane == 0) {
+            if (lg == 0 && valid) {
                 R.x -= C.x;
                 R.y -= C.y;
                 R.z -= C.z;
@@ -257,19 +263,19 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
         __syncthreads();
         // partials double-buffered by sweep parity: a CTA that runs ahead into the
         // next sweep cannot overwrite what a slower CTA is still summing
-        double* part = a.partial + (int64_t)(count & 1) * G * 4;
+        double* part = a.partial + (int64_t)(count & 1) * NB * 4;
         if (tid < 4) {
             double s = 0.0;
             for (int w = 0; w < kSmallBlock / 32; ++w) s = (tid == 3) ? fmax(s, red[3][w]) : s + red[tid][w];
             part[(int64_t)blockIdx.x * 4 + tid] = s;
         }
-        grid_barrier(G);
+        grid_barrier(NB);
         // warp 0 sums the CTA partials (lane l: CTAs l, l+32, ..., then a fixed
         // xor tree): the same order in every CTA; broadcast via shared memory
         __shared__ double s_tot[4];
         if (warp == 0) {
             double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-            for (unsigned b = lane; b < G; b += 32) {
+            for (unsigned b = lane; b < NB; b += 32) {
                 const double2 u = __ldcg(reinterpret_cast<const double2*>(part + (int64_t)b * 4));
                 const double2 v = __ldcg(reinterpret_cast<const double2*>(part + (int64_t)b * 4 + 2));
                 t0 += u.x;
@@ -342,9 +348,9 @@ __global__ void __launch_bounds__(kSmallBlock, 1) k_small_level(SmallArgs a) {
     }
 }
 
-template <int DIM, bool APPROX>
+template <int DIM, bool APPROX, int G>
 cudaError_t launch_small_t(const SmallArgs& a, int grid, size_t smem, cudaStream_t st) {
-    auto* fn = k_small_level<DIM, APPROX>;
+    auto* fn = k_small_level<DIM, APPROX, G>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     SmallArgs args = a;
@@ -366,15 +372,15 @@ int small_level_grid(int32_t n) {
         if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
         return v;
     }();
-    const int need = (int)((n + kSmallBlock / 32 - 1) / (kSmallBlock / 32));  // one warp per target
+    const int need = (int)((n + kSmallBlock / 32 - 1) / (kSmallBlock / 32));  // >= one warp per target
     return std::max(1, std::min(need, sms));
 }
 
 bool small_level_ok(int dim, int32_t n, int32_t k, bool approx) {
-    // measured crossover with the tiled path (profiles/README.md): ~8K targets
+    // measured crossover with the tiled path (profiles/README.md): ~25-40K targets
     static const int64_t max_n = [] {
         const char* e = getenv("MM_SMALL_N");  // 0 disables the persistent small-level path
-        return e ? (int64_t)atoll(e) : (int64_t)8192;
+        return e ? (int64_t)atoll(e) : (int64_t)32768;
     }();
     if (max_n <= 0 || n > max_n) return false;
     if (!approx && n > 4096) return false;                    // all n sources in shared memory
@@ -386,8 +392,21 @@ cudaError_t launch_small_level(int dim, bool approx, const SmallArgs& a, cudaStr
     const int grid = small_level_grid(a.n);
     const size_t smem = small_level_smem(dim, a.n, a.k, approx);
     LaunchScope ls("small_level", st);
-    if (dim == 2) return approx ? launch_small_t<2, true>(a, grid, smem, st) : launch_small_t<2, false>(a, grid, smem, st);
-    return approx ? launch_small_t<3, true>(a, grid, smem, st) : launch_small_t<3, false>(a, grid, smem, st);
+    // lanes per target: one or two targets per group per sweep
+    const int64_t lanes = (int64_t)grid * kSmallBlock;
+    const int G = (a.n * 32 <= 2 * lanes) ? 32 : (a.n * 16 <= 2 * lanes) ? 16 : 8;
+#define MM_S(D, AP)                                                              \
+    switch (G) {                                                                 \
+        case 32: return launch_small_t<D, AP, 32>(a, grid, smem, st);            \
+        case 16: return launch_small_t<D, AP, 16>(a, grid, smem, st);            \
+        default: return launch_small_t<D, AP, 8>(a, grid, smem, st);            \
+    }
+    if (dim == 2) {
+        if (approx) { MM_S(2, true) } else { MM_S(2, false) }
+    } else {
+        if (approx) { MM_S(3, true) } else { MM_S(3, false) }
+    }
+#undef MM_S
 }
 
 int small_level_partials(int32_t n) { return 2 * small_level_grid(n); }
