@@ -1,5 +1,5 @@
 """-m gpu: the persistent small-level kernel (k_small.cu) that runs all the
-sweeps of a level of up to 8,192 vertices (exact: 4,096) in one cooperative
+sweeps of a level of up to 32,768 vertices (exact: 4,096) in one cooperative
 launch.  mm_layout with one sweep at h = 0 goes through it for these sizes, so
 its first sweep is checked against the oracle's Eq.(2) sweep; K sweeps are
 checked against K oracle sweeps (Jacobi: each from the previous result); the
