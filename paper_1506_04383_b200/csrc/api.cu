@@ -1119,7 +1119,16 @@ mm_status run_small(const mm_sset* S, int dim, float q, const mm_approx* ap, con
     a.partial = sb.stat_partial;
     a.result = sb.flags;  // re-armed (memset) before the next level's sweeps
     a.stats = dstats;
-    MM_CU(launch_small_level(dim, ap != nullptr, a, ls), "small level");
+    {
+        const cudaError_t e = launch_small_level(dim, ap != nullptr, a, ls);
+        if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+            // the grid cannot be co-resident here (e.g. the GPU is shared): the
+            // caller runs the tiled path instead
+            cudaGetLastError();
+            return MM_ERR_UNSUPPORTED;
+        }
+        MM_CU(e, "small level");
+    }
     if (mode == 0) {
         *res = (K & 1) ? x1 : x0;
         *nsw = K;
@@ -1147,8 +1156,10 @@ struct FixedRunner : Runner {
                   mm_sweep_stats* dstats, const SweepBufs& sb, cudaStream_t ls, int32_t level, bool,
                   const float** res, int32_t* nsw) override {
         const int32_t K = sweeps[std::min(level, nsweeps - 1)];
-        if (K >= 1 && small_level_ok(dim, S->n, ap ? ap->k : 0, ap != nullptr))
-            return run_small(S, dim, q, ap, src, A, B, dstats, sb, ls, 0, K, alpha, nullptr, res, nsw);
+        if (K >= 1 && small_level_ok(dim, S->n, ap ? ap->k : 0, ap != nullptr)) {
+            const mm_status st = run_small(S, dim, q, ap, src, A, B, dstats, sb, ls, 0, K, alpha, nullptr, res, nsw);
+            if (st != MM_ERR_UNSUPPORTED) return st;
+        }
         MM_CU(run_sweeps(S, dim, alpha, q, ap, src, A, B, K, dstats, sb, ls, res), "mm_layout sweeps");
         *nsw = K;
         return MM_OK;
@@ -1363,9 +1374,11 @@ struct ScheduleRunner : Runner {
             const char* e = getenv("MM_SCHED_GRAPH");
             return !(e && e[0] == '0');
         }();
-        if (sch.a >= 1 && sch.max_final_iters >= 1 && small_level_ok(dim, S->n, ap ? ap->k : 0, ap != nullptr))
-            return run_small(S, dim, q, ap, src, A, B, dstats, sb, ls, 1, 0,
-                             start_at_min ? sch.alpha_min : sch.alpha0, &sch, res, nsw);
+        if (sch.a >= 1 && sch.max_final_iters >= 1 && small_level_ok(dim, S->n, ap ? ap->k : 0, ap != nullptr)) {
+            const mm_status st = run_small(S, dim, q, ap, src, A, B, dstats, sb, ls, 1, 0,
+                                           start_at_min ? sch.alpha_min : sch.alpha0, &sch, res, nsw);
+            if (st != MM_ERR_UNSUPPORTED) return st;
+        }
         if (dev_loop && graphs_enabled() && sch.a >= 1 && sch.max_final_iters >= 1)
             return run_graph(S, dim, q, ap, src, A, B, dstats, sb, ls, start_at_min, res, nsw);
         double alpha = start_at_min ? sch.alpha_min : sch.alpha0;
