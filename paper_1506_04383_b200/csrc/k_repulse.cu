@@ -612,7 +612,10 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
 }
 
 template <int DIM, bool QPOW, bool COARSE>
-constexpr int kBatchMask = (DIM == 2 && !QPOW) ? 1 : 0;  // measured: tools/ubench_repulse.cu
+#ifndef MM_COARSE_BMASK
+#define MM_COARSE_BMASK 0  // measured: plain reciprocals beat batching once nu is folded (+2%, cfg3)
+#endif
+constexpr int kBatchMask = (DIM == 2 && !QPOW) ? (COARSE ? MM_COARSE_BMASK : 1) : 0;  // measured: tools/ubench_repulse.cu
 
 template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
