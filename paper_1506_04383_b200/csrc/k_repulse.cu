@@ -218,6 +218,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
 // Kernel (a) adds, for vertex i of block B, its i-side slots and jpart[I][i]
 // for I < B, in that fixed order: the result is bitwise deterministic.
 constexpr int kSymTPB = 1024;  // vertices per block (targets = sources)
+#ifndef MM_SYM_BATCH
+#define MM_SYM_BATCH 0  // measured: plain reciprocals +2.8% (the symmetric mix is FMA-bound, MUFU 60%)
+#endif
+constexpr bool kSymBatch = MM_SYM_BATCH != 0;  // batched reciprocal in every other target group
 
 #ifndef MM_SYM_SRC
 #define MM_SYM_SRC 256
@@ -254,7 +258,7 @@ __device__ __forceinline__ void sym_chunk(const f2x (&X)[SG], const f2x (&Y)[SG]
                 dz = sub_bc(Z[gg], sz);
                 r2 = fma2(dz, dz, r2);
             }
-            f2x inv = (gg & 1) == 0 ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+            f2x inv = (kSymBatch && (gg & 1) == 0) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
             if constexpr (MASK) inv = mul2(inv, pk(sw, sw));
             AX[gg] = fma2(dx, inv, AX[gg]);
             AY[gg] = fma2(dy, inv, AY[gg]);
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(WARPS * 32, MM_SYM_MINB) k_repulse_sym(int32_t
                                 r2 = fma2(dz, dz, r2);
                             }
                             const f2x inv =
-                                (gg & 1) == 0 ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+                                (kSymBatch && (gg & 1) == 0) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
                             AX[gg] = fma2(dx, inv, AX[gg]);
                             AY[gg] = fma2(dy, inv, AY[gg]);
                             if constexpr (DIM == 3) AZ[gg] = fma2(dz, inv, AZ[gg]);
