@@ -295,7 +295,7 @@ __device__ __forceinline__ void sym_chunk(const f2x (&X)[SG], const f2x (&Y)[SG]
 }
 
 #ifndef MM_SYM_MINB
-#define MM_SYM_MINB 3
+#define MM_SYM_MINB 6
 #endif
 template <int DIM, bool QPOW, int SG, int WARPS, int SRC>
 __global__ void __launch_bounds__(WARPS * 32, MM_SYM_MINB) k_repulse_sym(int32_t n, const float* __restrict__ x, float cexp,
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(WARPS * 32, MM_SYM_MINB) k_repulse_sym(int32_t
 }
 
 #ifndef MM_SYM_SG
-#define MM_SYM_SG 2
+#define MM_SYM_SG 4  // 8 targets per lane, 4 warps per CTA (measured best with plain reciprocals)
 #endif
 constexpr int kSymSG = MM_SYM_SG;
 constexpr int kSymWarps = kSymTPB / (64 * kSymSG);
