@@ -745,7 +745,29 @@ mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uin
         } else {
         if (launch_fill(cur.n, -1, mate, st) != cudaSuccess) { set_err("mm_build_hierarchy: fill"); return fail(MM_ERR_CUDA); }
         int32_t rounds = max_rounds;
-        for (int32_t r = 0; r < max_rounds; ++r) {
+        bool device_loop = false;
+        {
+            // all rounds in one cooperative launch (host loop below if it cannot be resident)
+            const cudaError_t e = max_rounds > 0 ? run_match_level(cur.n, cur.nnz, cur.rp, cur.col, cur.omega, cur.c, mate,
+                                                                   cand, seed, (int32_t)li, max_rounds, added,
+                                                                   added + 2, st)
+                                                 : cudaErrorNotSupported;
+            if (e == cudaSuccess) {
+                device_loop = true;
+                if (cudaMemcpyAsync(&rounds, added + 2, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+                    cudaStreamSynchronize(st) != cudaSuccess) {
+                    set_err("mm_build_hierarchy: matching rounds d2h");
+                    return fail(MM_ERR_CUDA);
+                }
+            } else {
+                cudaGetLastError();
+                if (e != cudaErrorCooperativeLaunchTooLarge && e != cudaErrorNotSupported) {
+                    set_err("mm_build_hierarchy: matching: %s", cudaGetErrorString(e));
+                    return fail(MM_ERR_CUDA);
+                }
+            }
+        }
+        for (int32_t r = 0; r < max_rounds && !device_loop; ++r) {
             int32_t h_added = 0;
             if (cudaMemsetAsync(added, 0, 4, st) ||
                 run_match_round(cur.n, cur.nnz, cur.rp, cur.col, cur.omega, cur.c, mate, cand, seed, (int32_t)li, r, added, st) ||

@@ -85,6 +85,107 @@ __global__ void k_match_pick(int32_t n, const int64_t* __restrict__ rp, const in
     if (u < n && lg == 0) cand[u] = active ? best.v : -1;
 }
 
+// ---------------------------------------------------------------------------
+// All handshake rounds of one level in ONE cooperative launch (every CTA
+// resident; grid barriers between the phases): per round, pick (G lanes per
+// unmatched vertex, as k_match_pick) -> barrier -> confirm (mutual picks match,
+// counted) -> barrier -> every CTA reads the count and continues while a round
+// added a match and fewer than max_rounds ran.  Same rounds, same hashes, same
+// decisions as the host loop of k_match_pick / k_match_confirm launches.
+// Arrays written inside the launch (mate, cand, the counters) are read
+// through L2 (ld.global.cg), never the non-coherent path.
+struct MatchSync {
+    unsigned count;
+    unsigned gen;
+};
+__device__ MatchSync g_match_sync;
+
+__device__ __forceinline__ void match_grid_barrier(unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = &g_match_sync.gen;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(&g_match_sync.count, 1u) == nblocks - 1) {
+            g_match_sync.count = 0;
+            __threadfence();
+            atomicAdd(&g_match_sync.gen, 1u);
+        } else {
+            while (*gen == g) __nanosleep(40);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) k_match_level(int32_t n, const int64_t* __restrict__ rp,
+                                                     const int32_t* __restrict__ col, const int32_t* __restrict__ omega,
+                                                     const int32_t* __restrict__ c, int32_t* mate, int32_t* cand,
+                                                     uint64_t seed, int32_t level, int32_t max_rounds,
+                                                     int32_t* added /* [2], zeroed */, int32_t* rounds_out) {
+    const unsigned NB = gridDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x, nt = (int64_t)NB * blockDim.x;
+    const int lg = (int)(t0 & (G - 1));
+    const int64_t ngroups = nt / G;
+    const int64_t iters = ((int64_t)n + ngroups - 1) / ngroups;
+    __shared__ int32_t s_cnt;
+    int32_t round = 0;
+    for (;;) {
+        // ---- pick: G lanes per vertex, uniform trip count (the shuffles need every lane)
+        for (int64_t r = 0; r < iters; ++r) {
+            const int64_t uu = t0 / G + r * ngroups;
+            const int32_t u = (int32_t)(uu < n ? uu : n - 1);
+            Cand best{-1, 0, 1, 0};
+            const bool active = uu < n && __ldcg(mate + u) < 0;
+            if (active) {
+                const int64_t e1 = rp[u + 1];
+                for (int64_t e = rp[u] + lg; e < e1; e += G) {
+                    const int32_t v = col[e];
+                    if (v == u || __ldcg(mate + v) >= 0) continue;
+                    const Cand cv{v, omega ? omega[e] : 1, c[v], match_hash(seed, level, round, u, v)};
+                    if (cand_better(cv, best)) best = cv;
+                }
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) {
+                Cand other;
+                other.v = __shfl_xor_sync(0xffffffffu, best.v, o, G);
+                other.w = __shfl_xor_sync(0xffffffffu, best.w, o, G);
+                other.c = __shfl_xor_sync(0xffffffffu, best.c, o, G);
+                other.h = __shfl_xor_sync(0xffffffffu, best.h, o, G);
+                if (cand_better(other, best)) best = other;
+            }
+            if (uu < n && lg == 0) cand[u] = active ? best.v : -1;
+        }
+        match_grid_barrier(NB);
+        // the next round's counter: every CTA read it (as round - 1's) before this barrier
+        if (blockIdx.x == 0 && threadIdx.x == 0) added[(round + 1) & 1] = 0;
+        // ---- confirm: mutual picks match
+        if (threadIdx.x == 0) s_cnt = 0;
+        __syncthreads();
+        int32_t hit = 0;
+        for (int64_t u = t0; u < n; u += nt) {
+            if (__ldcg(mate + u) < 0) {
+                const int32_t v = __ldcg(cand + u);
+                if (v >= 0 && __ldcg(cand + v) == (int32_t)u) {
+                    mate[u] = v;
+                    ++hit;
+                }
+            }
+        }
+        hit = __reduce_add_sync(0xffffffffu, hit);
+        if ((threadIdx.x & 31) == 0 && hit) atomicAdd(&s_cnt, hit);
+        __syncthreads();
+        if (threadIdx.x == 0 && s_cnt) atomicAdd(added + (round & 1), s_cnt);
+        match_grid_barrier(NB);
+        const int32_t a = __ldcg(added + (round & 1));
+        ++round;
+        if (a == 0 || round >= max_rounds) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *rounds_out = round;
+}
+
 __global__ void k_match_confirm(int32_t n, const int32_t* __restrict__ cand, int32_t* __restrict__ mate,
                                 int32_t* __restrict__ added) {
     const int32_t u = blockIdx.x * blockDim.x + threadIdx.x;
@@ -383,6 +484,36 @@ cudaError_t run_match_round(int32_t n, int64_t nnz, const int64_t* rp, const int
         k_match_confirm<<<nblk(n), 256, 0, st>>>(n, cand, mate, added);
     }
     return cudaGetLastError();
+}
+
+template <int G>
+cudaError_t match_level_t(int32_t n, const int64_t* rp, const int32_t* col, const int32_t* omega, const int32_t* c,
+                          int32_t* mate, int32_t* cand, uint64_t seed, int32_t level, int32_t max_rounds,
+                          int32_t* added, int32_t* rounds_out, cudaStream_t st) {
+    static const int grid = [] {
+        int dev = 0, sms = 148, occ = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_match_level<G>, 256, 0);
+        return sms * std::max(occ, 1);
+    }();
+    void* params[] = {&n, &rp, &col, &omega, &c, &mate, &cand, &seed, &level, &max_rounds, &added, &rounds_out};
+    return cudaLaunchCooperativeKernel((const void*)k_match_level<G>, dim3(grid), dim3(256), params, 0, st);
+}
+
+cudaError_t run_match_level(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
+                            const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
+                            int32_t max_rounds, int32_t* added, int32_t* rounds_out, cudaStream_t st) {
+    LaunchScope ls("match_level", st);
+    cudaError_t e = cudaMemsetAsync(added, 0, 2 * sizeof(int32_t), st);
+    if (e != cudaSuccess) return e;
+    switch (match_group(n, nnz)) {
+        case 2: return match_level_t<2>(n, rp, col, omega, c, mate, cand, seed, level, max_rounds, added, rounds_out, st);
+        case 4: return match_level_t<4>(n, rp, col, omega, c, mate, cand, seed, level, max_rounds, added, rounds_out, st);
+        case 8: return match_level_t<8>(n, rp, col, omega, c, mate, cand, seed, level, max_rounds, added, rounds_out, st);
+        case 16: return match_level_t<16>(n, rp, col, omega, c, mate, cand, seed, level, max_rounds, added, rounds_out, st);
+        default: return match_level_t<32>(n, rp, col, omega, c, mate, cand, seed, level, max_rounds, added, rounds_out, st);
+    }
 }
 
 cudaError_t launch_fill(int64_t n, int32_t v, int32_t* a, cudaStream_t st) {

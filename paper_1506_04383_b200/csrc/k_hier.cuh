@@ -7,6 +7,11 @@ namespace mm {
 cudaError_t run_match_round(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
                             const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
                             int32_t round, int32_t* added, cudaStream_t st);
+// all handshake rounds of one level in one cooperative launch; *rounds_out (device) = rounds run;
+// added: device int32[2] scratch.  cudaErrorCooperativeLaunchTooLarge: use run_match_round instead
+cudaError_t run_match_level(int32_t n, int64_t nnz, const int64_t* rp, const int32_t* col, const int32_t* omega,
+                            const int32_t* c, int32_t* mate, int32_t* cand, uint64_t seed, int32_t level,
+                            int32_t max_rounds, int32_t* added, int32_t* rounds_out, cudaStream_t st);
 cudaError_t launch_fill(int64_t n, int32_t v, int32_t* a, cudaStream_t st);
 size_t scan_temp_bytes(int32_t n);
 size_t sort_temp_bytes_u64(int64_t m);
