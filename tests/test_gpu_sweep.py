@@ -298,3 +298,17 @@ def test_caller_workspace_bitwise(mm, name, approx):
     assert torch.equal(a, b)
     with pytest.raises(mm.MMError):
         mm.sweep(S, xd, w.alpha, w.q, workspace=ws[:64], **kw)
+
+
+@pytest.mark.parametrize("n,q", [(30001, 0.8), (25000, 0.0)])
+def test_exact_sweep_3d_symmetric_sampled(mm, n, q):
+    """3-D exact sweeps above the symmetric kernel's threshold (n >~ 21K), so
+    the default path takes it; 1,024 sampled rows against the oracle."""
+    assert mm.exact_kernel_variant(n, 3) == 1
+    g = H.random_connected(n, n // 2 + 1, seed=n)
+    S = sset.hop2_sset(g)
+    x = configs.random_state(n, 3, seed=n + 3, scale=n ** (1 / 3))
+    got = _gpu_sweep(mm, S, x, 0.05, q)
+    rows = sample_rows(n, 1024, seed=11)
+    want = oracle.sweep_exact(S, x.astype(np.float64), 0.05, q, rows=rows)
+    assert_sweep_parity(got[rows], want, f"3-D n={n} q={q}")
