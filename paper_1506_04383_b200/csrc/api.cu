@@ -221,6 +221,9 @@ struct SweepBufs {
     int32_t* key_sorted = nullptr;
     int32_t* iota = nullptr;
     int32_t* cnt = nullptr;
+    int32_t* rord = nullptr;     // representatives in mass order (Q26): slot -> rep id
+    int32_t* rpos = nullptr;     // rep id -> slot
+    int32_t* tile_nu = nullptr;  // [ceil(k / kCoarseTile)] common mass of a tile, or 0
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
 };
@@ -274,6 +277,7 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
         b += 2 * al((size_t)k * sizeof(float4)) + al((size_t)(k + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)(n + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)n * 4) * 2 + al((size_t)(std::max(n, k) + 2) * 4);
+        b += 2 * al((size_t)k * 4) + al((size_t)(k / kCoarseTile + 1) * 4);
         b += al(cub_tmp_bytes(n));
     }
     return b + 4096;
@@ -297,6 +301,9 @@ bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double 
         sb.key_sorted = cv.take<int32_t>(n);
         sb.iota = cv.take<int32_t>(n);
         sb.cnt = cv.take<int32_t>(std::max(n, k) + 2);
+        sb.rord = cv.take<int32_t>(k);
+        sb.rpos = cv.take<int32_t>(k);
+        sb.tile_nu = cv.take<int32_t>(k / kCoarseTile + 1);
         sb.tmp_bytes = cub_tmp_bytes(n);
         sb.tmp = cv.take<char>(sb.tmp_bytes);
     }
@@ -308,8 +315,12 @@ cudaError_t prepare_approx(int32_t n, const mm_approx* ap, SweepBufs& sb, cudaSt
     cudaError_t e = group_by_key(n, ap->ancestor, ap->k, sb.mptr, sb.mem, sb.key_sorted, sb.iota, sb.cnt, sb.tmp,
                                  sb.tmp_bytes, st);
     if (e != cudaSuccess) return e;
-    return group_by_key(n, ap->parent, n, sb.cptr, sb.child, sb.key_sorted, sb.iota, sb.cnt, sb.tmp, sb.tmp_bytes,
-                        st);
+    e = group_by_key(n, ap->parent, n, sb.cptr, sb.child, sb.key_sorted, sb.iota, sb.cnt, sb.tmp, sb.tmp_bytes, st);
+    if (e != cudaSuccess || coarse_excludes_own()) return e;
+    // representatives in mass order, so kernel (c) scales whole tiles by nu (Q26);
+    // group_by_key left iota = 0..n-1 (k <= n)
+    return rep_mass_order(ap->k, sb.mptr, kCoarseTile, sb.cnt, sb.key_sorted, sb.iota, sb.rord, sb.rpos, sb.tile_nu,
+                          sb.tmp, sb.tmp_bytes, st);
 }
 
 // One sweep with all buffers prepared (graph-capturable: no allocation, no sync).
@@ -323,16 +334,19 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     RepulsePlan p;
     SymPlan sp;
     if (ap) {
-        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rep_hi, sb.rep_lo, st);
+        const bool mass_order = !coarse_excludes_own();
+        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, mass_order ? sb.rord : nullptr, sb.rep_hi,
+                            sb.rep_lo, st);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
-        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, ap->ancestor, p, sb.part, st);
+        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, ap->ancestor,
+                           mass_order ? sb.tile_nu : nullptr, p, sb.part, st);
     } else if (sb.jpart) {
         sp = plan_repulse_sym(n, dim);
         e = launch_repulse_sym(dim, qpow, q, n, x_in, sp, sb.part, sb.jpart, st);
     } else {
         p = plan_repulse(n, n, dim, false, qpow);
-        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, nullptr, p, sb.part, st);
+        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, nullptr, nullptr, p, sb.part, st);
     }
     if (e != cudaSuccess) return e;
     GatherArgs ga;
@@ -356,6 +370,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     }
     if (ap && !coarse_excludes_own()) {
         ga.anc = ap->ancestor;
+        ga.rpos = sb.rpos;
         ga.rep_hi = sb.rep_hi;
         ga.rep_lo = sb.rep_lo;
     }
@@ -957,7 +972,7 @@ bool graphs_enabled() {
 // captured launches depend on (pointers, sizes, parameters).  A hit relaunches
 // the executable graph; capture + instantiate is paid once per distinct key.
 struct GraphKey {
-    const void* p[17];
+    const void* p[20];
     int64_t v[8];
     float f[2];
     int32_t kind = 0;      // 0: K fixed sweeps; 1: device-driven schedule loop of one level
@@ -1009,8 +1024,9 @@ GraphKey make_key(const mm_sset* S, int dim, float alpha, float q, const mm_appr
     GraphKey k;
     memset(&k, 0, sizeof(k));
     (void)st;  // an executable graph may be launched into any stream
-    const void* ps[17] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
-                          sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child, sb.jpart};
+    const void* ps[20] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
+                          sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child, sb.jpart,
+                          sb.rord, sb.rpos, sb.tile_nu};
     memcpy(k.p, ps, sizeof(ps));
     k.v[0] = S->n;
     k.v[1] = S->nnz;

@@ -142,7 +142,8 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 // Eq.(3) excludes the own representative H(i); kernel (c)
                 // summed all k, so its term goes into C (subtracted), computed with
                 // kernel (c)'s hi/lo differencing (Q25)
-                const int32_t h = __ldg(a.anc + i);
+                int32_t h = __ldg(a.anc + i);
+                if (a.rpos != nullptr) h = __ldg(a.rpos + h);
                 const float4 rh = __ldg(a.rep_hi + h), rl = __ldg(a.rep_lo + h);
                 const float dx = (xi.x - rh.x) - rl.x, dy = (xi.y - rh.y) - rl.y;
                 float r2 = fmaf(dx, dx, kEps2);

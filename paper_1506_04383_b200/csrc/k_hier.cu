@@ -319,9 +319,11 @@ __global__ void k_compose(int32_t n, const int32_t* __restrict__ a, const int32_
 // lane l sums members l, l+G, ... in order, then a fixed shuffle tree.
 template <int DIM, int G>
 __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
-                           const float* __restrict__ x, float4* __restrict__ rep_hi, float4* __restrict__ rep_lo) {
+                           const float* __restrict__ x, const int32_t* __restrict__ rord,
+                           float4* __restrict__ rep_hi, float4* __restrict__ rep_lo) {
     const int64_t tg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int32_t v = (int32_t)(tg / G);
+    const int32_t slot = (int32_t)(tg / G);
+    const int32_t v = (rord != nullptr && slot < k) ? __ldg(rord + slot) : slot;
     const int lg = (int)(tg & (G - 1));
     double sx = 0.0, sy = 0.0, sz = 0.0;
     int32_t b = 0, e = 0;
@@ -341,12 +343,29 @@ __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const in
         sy += __shfl_xor_sync(0xffffffffu, sy, o, G);
         if constexpr (DIM == 3) sz += __shfl_xor_sync(0xffffffffu, sz, o, G);
     }
-    if (v >= k || lg != 0) return;
+    if (slot >= k || lg != 0) return;
     const double nu = (double)(e - b);
     const double mx = sx / nu, my = sy / nu, mz = DIM == 3 ? sz / nu : 0.0;
     const float hx = (float)mx, hy = (float)my, hz = (float)mz;
-    rep_hi[v] = make_float4(hx, hy, hz, (float)nu);
-    rep_lo[v] = make_float4((float)(mx - hx), (float)(my - hy), (float)(mz - hz), 0.f);
+    rep_hi[slot] = make_float4(hx, hy, hz, (float)nu);
+    rep_lo[slot] = make_float4((float)(mx - hx), (float)(my - hy), (float)(mz - hz), 0.f);
+}
+
+// Mass order of the representatives (Q26): nu(v) = member count
+__global__ void k_rep_mass(int32_t k, const int32_t* __restrict__ mptr, int32_t* __restrict__ nu) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v < k) nu[v] = mptr[v + 1] - mptr[v];
+}
+// rpos = inverse of rord; tile_nu[t] = the common mass of slots [256 t, 256 t + 255] or 0
+__global__ void k_rep_slots(int32_t k, const int32_t* __restrict__ rord, const int32_t* __restrict__ nu_sorted,
+                            int32_t* __restrict__ rpos, int32_t* __restrict__ tile_nu, int tile) {
+    const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= k) return;
+    rpos[rord[s]] = s;
+    if (s % tile == 0) {
+        const int32_t last = min(s + tile - 1, k - 1);
+        tile_nu[s / tile] = nu_sorted[s] == nu_sorted[last] ? nu_sorted[s] : 0;
+    }
 }
 
 template <int DIM>
@@ -642,8 +661,27 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
     return cudaGetLastError();
 }
 
+cudaError_t rep_mass_order(int32_t k, const int32_t* mptr, int tile, int32_t* nu, int32_t* nu_sorted,
+                           const int32_t* iota, int32_t* rord, int32_t* rpos, int32_t* tile_nu, void* tmp,
+                           size_t tmp_bytes, cudaStream_t st) {
+    if (k <= 0) return cudaSuccess;
+    {
+        LaunchScope ls("rep_mass", st);
+        k_rep_mass<<<nblk(k), 256, 0, st>>>(k, mptr, nu);
+    }
+    {
+        LaunchScope ls("cub_sort_mass", st);
+        // stable: equal masses keep representative-id order
+        const cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, nu, nu_sorted, iota, rord, k, 0, 31, st);
+        if (e != cudaSuccess) return e;
+    }
+    LaunchScope ls("rep_slots", st);
+    k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, nu_sorted, rpos, tile_nu, tile);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                            float4* rep_hi, float4* rep_lo, cudaStream_t st) {
+                            const int32_t* rord, float4* rep_hi, float4* rep_lo, cudaStream_t st) {
     LaunchScope ls("centroid", st);
     // lanes per representative: about 4 members per lane
     const double mean = k > 0 ? (double)n / k : 1.0;
@@ -652,12 +690,12 @@ cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, 
     const int nb = nblk((int64_t)k * G);
 #define MM_C(D)                                                                               \
     switch (G) {                                                                              \
-        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
-        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
-        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
-        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break;   \
-        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break; \
-        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rep_hi, rep_lo); break; \
+        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
+        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
+        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
+        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
+        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break; \
+        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break; \
     }
     if (dim == 2) { MM_C(2) } else { MM_C(3) }
 #undef MM_C

@@ -36,6 +36,7 @@ namespace mm {
 namespace {
 
 constexpr int kBlock = 256;   // threads per CTA = sources per shared-memory tile
+static_assert(kBlock == kCoarseTile, "tile_nu granularity");
 
 // 1/|d|^(q+2) for a packed pair of r^2.  q = 0 batched: one MUFU for both,
 // 1/a = b * rcp(a*b), 1/b = a * rcp(a*b) (FMUL + MUFU + FMUL2 with swapped halves).
@@ -54,11 +55,82 @@ __device__ __forceinline__ f2x inv_pair(f2x r2, float cexp) {
 #ifndef MM_COARSE_MASK
 #define MM_COARSE_MASK 0  // 1: exclude H(i) inside kernel (c) (experiments; round-1 design)
 #endif
+// One shared-memory source tile against the thread's T = 2G targets: T* += the
+// pair terms.  PAIR_NU: multiply every pair by its representative's mass nu
+// (coarse tiles of mixed mass); otherwise the caller scales the tile sum.
+template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, int UNR, bool PAIR_NU>
+__device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const float4* sm_b, const f2x (&X)[G],
+                                           const f2x (&Y)[G], const f2x (&Z)[G], f2x (&TX)[G], f2x (&TY)[G],
+                                           f2x (&TZ)[G], float cexp, const int32_t* hi, int64_t t0) {
+    const f2x eps2 = pk(kEps2, kEps2);
+    const float2* sm2 = reinterpret_cast<const float2*>(sm_a);
+    (void)hi;
+    (void)t0;
+#pragma unroll UNR
+    for (int jj = 0; jj < cnt; ++jj) {
+        float sx, sy, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f, nu = 1.f;
+        if constexpr (COARSE) {
+            const float4 a = sm_a[jj], b = sm_b[jj];
+            sx = a.x; sy = a.y; sz = a.z; nu = a.w;
+            lx = b.x; ly = b.y; lz = b.z;
+        } else if constexpr (DIM == 2) {
+            const float2 a = sm2[jj];
+            sx = a.x; sy = a.y;
+        } else {
+            const float4 a = sm_a[jj];
+            sx = a.x; sy = a.y; sz = a.z;
+        }
+        (void)nu;
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+            f2x dx = sub_bc(X[gg], sx);
+            f2x dy = sub_bc(Y[gg], sy);
+            if constexpr (COARSE) {
+                dx = sub_bc(dx, lx);
+                dy = sub_bc(dy, ly);
+            }
+            f2x r2 = fma2(dx, dx, eps2);
+            r2 = fma2(dy, dy, r2);
+            f2x dz = 0ull;
+            if constexpr (DIM == 3) {
+                dz = sub_bc(Z[gg], sz);
+                if constexpr (COARSE) dz = sub_bc(dz, lz);
+                r2 = fma2(dz, dz, r2);
+            }
+            // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
+            f2x inv;
+            if constexpr (PAIR_NU && !MM_COARSE_MASK) {
+                // all k representatives, the own one H(i) included: kernel (a)
+                // subtracts that term (Q25); nu folded into the
+                // batched reciprocal: nu/a = b * (nu * rcp(ab))
+                if ((BMASK >> gg) & 1) {
+                    float r0, r1;
+                    upk(r2, r0, r1);
+                    const float ip = nu * rcp_approx(r0 * r1);
+                    inv = mul_bc(pk(r1, r0), ip);
+                } else {
+                    inv = mul_bc(inv_pair<QPOW, false>(r2, cexp), nu);
+                }
+            } else {
+                inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+            }
+            if constexpr (COARSE && MM_COARSE_MASK) {
+                const int32_t j = (int32_t)(t0 + jj);
+                inv = mul2(inv, pk(j == hi[2 * gg] ? 0.f : nu, j == hi[2 * gg + 1] ? 0.f : nu));
+            }
+            TX[gg] = fma2(dx, inv, TX[gg]);
+            TY[gg] = fma2(dy, inv, TY[gg]);
+            if constexpr (DIM == 3) TZ[gg] = fma2(dz, inv, TZ[gg]);
+        }
+    }
+}
+
 template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4>
 __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
                                                     const float4* __restrict__ rep_hi,
                                                     const float4* __restrict__ rep_lo,
-                                                    const int32_t* __restrict__ anc, float cexp, Sched sch,
+                                                    const int32_t* __restrict__ anc,
+                                                    const int32_t* __restrict__ tile_nu, float cexp, Sched sch,
                                                     float* __restrict__ part) {
     static_assert(T % 2 == 0, "targets are processed in packed pairs");
     constexpr int G = T / 2;
@@ -72,7 +144,6 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
     const int tid = threadIdx.x;
     const int32_t g = blockIdx.x;
     const int64_t u0 = (int64_t)g * sch.U / sch.G, u1 = (int64_t)(g + 1) * sch.U / sch.G;
-    const f2x eps2 = pk(kEps2, kEps2);
 
     for (int64_t u = u0; u < u1;) {
         const int32_t tb = (int32_t)(u / sch.Ub);
@@ -120,67 +191,29 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             f2x TX[G], TY[G], TZ[G];
 #pragma unroll
             for (int gg = 0; gg < G; ++gg) TX[gg] = TY[gg] = TZ[gg] = 0ull;
-#pragma unroll UNR
-            for (int jj = 0; jj < cnt; ++jj) {
-                float sx, sy, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f, nu = 1.f;
-                if constexpr (COARSE) {
-                    const float4 a = sm_a[jj], b = sm_b[jj];
-                    sx = a.x; sy = a.y; sz = a.z; nu = a.w;
-                    lx = b.x; ly = b.y; lz = b.z;
-                } else if constexpr (DIM == 2) {
-                    const float2 a = sm2[jj];
-                    sx = a.x; sy = a.y;
-                } else {
-                    const float4 a = sm_a[jj];
-                    sx = a.x; sy = a.y; sz = a.z;
-                }
+            // coarse tiles whose representatives all have the same mass nu
+            // (representatives are stored in mass order, Q26) sum
+            // (x_i - x')/|x_i - x'|^(q+2) and scale the tile sum by nu once
+            const int tnu = (COARSE && tile_nu != nullptr) ? __ldg(tile_nu + tile) : 0;
+            if (tnu > 0) {
+                tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, false>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp, hi,
+                                                                   t0);
+                const f2x nu2 = pk((float)tnu, (float)tnu);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
-                    f2x dx = sub_bc(X[gg], sx);
-                    f2x dy = sub_bc(Y[gg], sy);
-                    if constexpr (COARSE) {
-                        dx = sub_bc(dx, lx);
-                        dy = sub_bc(dy, ly);
-                    }
-                    f2x r2 = fma2(dx, dx, eps2);
-                    r2 = fma2(dy, dy, r2);
-                    f2x dz = 0ull;
-                    if constexpr (DIM == 3) {
-                        dz = sub_bc(Z[gg], sz);
-                        if constexpr (COARSE) dz = sub_bc(dz, lz);
-                        r2 = fma2(dz, dz, r2);
-                    }
-                    // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
-                    f2x inv;
-                    if constexpr (COARSE && !MM_COARSE_MASK) {
-                        // all k representatives, the own one H(i) included: kernel (a)
-                        // subtracts that term (Q25); nu folded into the
-                        // batched reciprocal: nu/a = b * (nu * rcp(ab))
-                        if ((BMASK >> gg) & 1) {
-                            float r0, r1;
-                            upk(r2, r0, r1);
-                            const float ip = nu * rcp_approx(r0 * r1);
-                            inv = mul_bc(pk(r1, r0), ip);
-                        } else {
-                            inv = mul_bc(inv_pair<QPOW, false>(r2, cexp), nu);
-                        }
-                    } else {
-                        inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
-                    }
-                    if constexpr (COARSE && MM_COARSE_MASK) {
-                        const int32_t j = (int32_t)(t0 + jj);
-                        inv = mul2(inv, pk(j == hi[2 * gg] ? 0.f : nu, j == hi[2 * gg + 1] ? 0.f : nu));
-                    }
-                    TX[gg] = fma2(dx, inv, TX[gg]);
-                    TY[gg] = fma2(dy, inv, TY[gg]);
-                    if constexpr (DIM == 3) TZ[gg] = fma2(dz, inv, TZ[gg]);
+                    AX[gg] = fma2(TX[gg], nu2, AX[gg]);
+                    AY[gg] = fma2(TY[gg], nu2, AY[gg]);
+                    if constexpr (DIM == 3) AZ[gg] = fma2(TZ[gg], nu2, AZ[gg]);
                 }
-            }
+            } else {
+                tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp, hi,
+                                                                    t0);
 #pragma unroll
-            for (int gg = 0; gg < G; ++gg) {
-                AX[gg] = add2(AX[gg], TX[gg]);
-                AY[gg] = add2(AY[gg], TY[gg]);
-                if constexpr (DIM == 3) AZ[gg] = add2(AZ[gg], TZ[gg]);
+                for (int gg = 0; gg < G; ++gg) {
+                    AX[gg] = add2(AX[gg], TX[gg]);
+                    AY[gg] = add2(AY[gg], TY[gg]);
+                    if constexpr (DIM == 3) AZ[gg] = add2(AZ[gg], TZ[gg]);
+                }
             }
         }
         // partial of this (target block, CTA) pair -> slot g - first CTA of the block
@@ -680,14 +713,15 @@ RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, boo
 
 cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_tgt, const float* x,
                            int32_t n_src, const float4* rep_hi, const float4* rep_lo, const int32_t* anc,
-                           const RepulsePlan& p, float* part, cudaStream_t st) {
+                           const int32_t* tile_nu, const RepulsePlan& p, float* part, cudaStream_t st) {
     const float cexp = -(q + 2.0f) * 0.5f;
     LaunchScope ls(coarse ? "repulse_coarse" : "repulse_exact", st);
 // batched reciprocals (BMASK) in half of the target groups for 2-D q = 0
 // (exact and coarse: measured faster by tools/ubench_repulse.cu); none for q > 0.
 #define MM_LAUNCH(D, Q, C, T) \
     k_repulse<D, Q, C, T, kBatchMask<D, Q, C>><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, anc, \
-                                                                          cexp, p.sch, part)
+                                                                          MM_COARSE_MASK ? nullptr : tile_nu, cexp,  \
+                                                                          p.sch, part)
     if (dim == 2) {
         if (!qpow && !coarse) MM_LAUNCH(2, false, false, 4);
         else if (!qpow && coarse) MM_LAUNCH(2, false, true, 4);

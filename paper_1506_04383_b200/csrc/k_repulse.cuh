@@ -57,7 +57,10 @@ int repulse_targets_per_block(int dim);
 bool coarse_excludes_own();  // kernel (c) built with MM_COARSE_MASK = 1
 cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_tgt, const float* x,
                            int32_t n_src, const float4* rep_hi, const float4* rep_lo, const int32_t* anc,
+                           const int32_t* tile_nu /* nullable: [ceil(n_src/256)] mass of a uniform-mass tile, else 0 */,
                            const RepulsePlan& p, float* part, cudaStream_t st);
+// sources per tile of the coarse kernel (granularity of tile_nu)
+constexpr int kCoarseTile = 256;
 EntropyPlan plan_entropy(int32_t n);
 cudaError_t launch_entropy_all(int dim, double q, int32_t n, const float* x, const EntropyPlan& p,
                                double* partial, int32_t* coinc, cudaStream_t st);
@@ -84,6 +87,7 @@ struct GatherArgs {
     // all k representatives (nullable: exact mode, or kernel (c) built with
     // MM_COARSE_MASK = 1)
     const int32_t* anc = nullptr;
+    const int32_t* rpos = nullptr;  // nullable: slot of representative v in rep_hi/rep_lo (mass order)
     const float4* rep_hi = nullptr;
     const float4* rep_lo = nullptr;
     // Eq.(3) sibling term (nullable: exact mode)
