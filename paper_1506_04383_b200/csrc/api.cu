@@ -224,12 +224,18 @@ struct SweepBufs {
     int32_t* rord = nullptr;     // representatives in mass order (Q26): slot -> rep id
     int32_t* rpos = nullptr;     // rep id -> slot
     int32_t* tile_nu = nullptr;  // [ceil(k / kCoarseTile)] common mass of a tile, or 0
+    int32_t* tperm = nullptr;    // targets in spatial order (Q27): slot -> vertex
+    int32_t* tpos = nullptr;     // vertex -> slot
+    float4* tile_box = nullptr;  // [2 ceil(k / kCoarseTile)] per-tile box of the representatives
+    uint64_t* rkey = nullptr;    // [2k] representative sort keys (scratch)
+    uint32_t* box = nullptr;     // [8] layout box (scratch)
+    bool reorder = false;        // recompute kernel (c)'s orders before every sweep
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
 };
 
 size_t cub_tmp_bytes(int32_t n) {
-    return std::max(sort_temp_bytes_i32(n), scan_temp_bytes(n + 2)) + 256;
+    return std::max({sort_temp_bytes_i32(n), sort_temp_bytes_u64(n), scan_temp_bytes(n + 2)}) + 256;
 }
 
 // Exact sweeps use the symmetric kernel (each unordered pair once)
@@ -278,6 +284,7 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
         b += al((size_t)(n + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)n * 4) * 2 + al((size_t)(std::max(n, k) + 2) * 4);
         b += 2 * al((size_t)k * 4) + al((size_t)(k / kCoarseTile + 1) * 4);
+        b += 2 * al((size_t)n * 4) + al((size_t)(k / kCoarseTile + 1) * 32) + al((size_t)k * 16) + al(32);
         b += al(cub_tmp_bytes(n));
     }
     return b + 4096;
@@ -304,23 +311,57 @@ bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double 
         sb.rord = cv.take<int32_t>(k);
         sb.rpos = cv.take<int32_t>(k);
         sb.tile_nu = cv.take<int32_t>(k / kCoarseTile + 1);
+        sb.tperm = cv.take<int32_t>(n);
+        sb.tpos = cv.take<int32_t>(n);
+        sb.tile_box = cv.take<float4>((size_t)2 * (k / kCoarseTile + 1));
+        sb.rkey = cv.take<uint64_t>((size_t)2 * k);
+        sb.box = cv.take<uint32_t>(8);
         sb.tmp_bytes = cub_tmp_bytes(n);
         sb.tmp = cv.take<char>(sb.tmp_bytes);
     }
     return cv.ok;
 }
 
+// Q27 switch: kernel (c) drops the lo correction on tiles far from a warp's
+// targets (MM_FAR_TILES=0 keeps hi/lo differencing everywhere; experiments)
+bool far_tiles() {
+    static const bool on = [] {
+        const char* v = getenv("MM_FAR_TILES");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// Kernel (c)'s orders from the positions x: targets in Morton order, representatives
+// by (mass, Morton) so that it scales whole tiles by nu (Q26) and drops the lo
+// correction on tiles far from a warp's targets (Q27).  group_by_key left
+// iota = 0..n-1 (k <= n); cnt / key_sorted are free scratch after prepare_approx.
+cudaError_t coarse_orders(int32_t n, int dim, const mm_approx* ap, const float* x, const SweepBufs& sb,
+                          cudaStream_t st) {
+    return approx_orders(dim, n, ap->k, sb.mptr, sb.mem, x, kCoarseTile, sb.iota, sb.box,
+                         reinterpret_cast<uint32_t*>(sb.cnt), reinterpret_cast<uint32_t*>(sb.key_sorted), sb.tperm,
+                         sb.tpos, sb.rkey, sb.rkey + ap->k, sb.rord, sb.rpos, sb.tile_nu, sb.tmp, sb.tmp_bytes, st);
+}
+
+// Re-sort before every sweep when kernel (c)'s work (n k pairs) dwarfs the two
+// sorts; otherwise once per level / mm_sweep call (MM_REORDER_PAIRS overrides)
+bool reorder_every_sweep(int32_t n, int32_t k) {
+    static const double thr = [] {
+        const char* v = getenv("MM_REORDER_PAIRS");
+        return v ? atof(v) : 1e11;  // measured: cfg4's finest level +2%, cfg3 (2e10) loses 5%
+    }();
+    return (double)n * (double)k >= thr;
+}
+
 // Group maps into CSRs (members of each representative, children of each parent).
-cudaError_t prepare_approx(int32_t n, const mm_approx* ap, SweepBufs& sb, cudaStream_t st) {
+cudaError_t prepare_approx(int32_t n, int dim, const mm_approx* ap, const float* x, SweepBufs& sb, cudaStream_t st) {
     cudaError_t e = group_by_key(n, ap->ancestor, ap->k, sb.mptr, sb.mem, sb.key_sorted, sb.iota, sb.cnt, sb.tmp,
                                  sb.tmp_bytes, st);
     if (e != cudaSuccess) return e;
     e = group_by_key(n, ap->parent, n, sb.cptr, sb.child, sb.key_sorted, sb.iota, sb.cnt, sb.tmp, sb.tmp_bytes, st);
-    if (e != cudaSuccess || coarse_excludes_own()) return e;
-    // representatives in mass order, so kernel (c) scales whole tiles by nu (Q26);
-    // group_by_key left iota = 0..n-1 (k <= n)
-    return rep_mass_order(ap->k, sb.mptr, kCoarseTile, sb.cnt, sb.key_sorted, sb.iota, sb.rord, sb.rpos, sb.tile_nu,
-                          sb.tmp, sb.tmp_bytes, st);
+    if (e != cudaSuccess) return e;
+    sb.reorder = reorder_every_sweep(n, ap->k);
+    return coarse_orders(n, dim, ap, x, sb, st);
 }
 
 // One sweep with all buffers prepared (graph-capturable: no allocation, no sync).
@@ -334,19 +375,25 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     RepulsePlan p;
     SymPlan sp;
     if (ap) {
-        const bool mass_order = !coarse_excludes_own();
-        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, mass_order ? sb.rord : nullptr, sb.rep_hi,
-                            sb.rep_lo, st);
+        if (sb.reorder) {
+            e = coarse_orders(n, dim, ap, x_in, sb, st);
+            if (e != cudaSuccess) return e;
+        }
+        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, sb.rep_hi, sb.rep_lo,
+                            far_tiles() ? sb.tile_box : nullptr, kCoarseTile, st);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
-        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, ap->ancestor,
-                           mass_order ? sb.tile_nu : nullptr, p, sb.part, st);
+        CoarseOrder co;
+        co.tperm = sb.tperm;
+        co.tile_nu = sb.tile_nu;
+        co.tile_box = far_tiles() ? sb.tile_box : nullptr;
+        e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, co, p, sb.part, st);
     } else if (sb.jpart) {
         sp = plan_repulse_sym(n, dim);
         e = launch_repulse_sym(dim, qpow, q, n, x_in, sp, sb.part, sb.jpart, st);
     } else {
         p = plan_repulse(n, n, dim, false, qpow);
-        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, nullptr, nullptr, p, sb.part, st);
+        e = launch_repulse(dim, qpow, false, q, n, x_in, n, nullptr, nullptr, CoarseOrder{}, p, sb.part, st);
     }
     if (e != cudaSuccess) return e;
     GatherArgs ga;
@@ -368,9 +415,10 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         ga.tri = sp.ts;
         ga.tpb = 1024;
     }
-    if (ap && !coarse_excludes_own()) {
+    if (ap) {
         ga.anc = ap->ancestor;
         ga.rpos = sb.rpos;
+        ga.tpos = sb.tpos;
         ga.rep_hi = sb.rep_hi;
         ga.rep_lo = sb.rep_lo;
     }
@@ -521,7 +569,7 @@ mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const mm_app
         return MM_ERR_INVALID_ARGUMENT;
     }
     MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), st), "mm_sweep memset");
-    if (ap) MM_CU(prepare_approx(n, ap, sb, st), "mm_sweep prepare_approx");
+    if (ap) MM_CU(prepare_approx(n, dim, ap, x_in, sb, st), "mm_sweep prepare_approx");
     MM_CU(sweep_core(S, dim, alpha, q, ap, x_in, x_out, stats, sb, st), "mm_sweep");
     return MM_OK;
 }
@@ -972,7 +1020,7 @@ bool graphs_enabled() {
 // captured launches depend on (pointers, sizes, parameters).  A hit relaunches
 // the executable graph; capture + instantiate is paid once per distinct key.
 struct GraphKey {
-    const void* p[20];
+    const void* p[23];
     int64_t v[8];
     float f[2];
     int32_t kind = 0;      // 0: K fixed sweeps; 1: device-driven schedule loop of one level
@@ -1024,9 +1072,9 @@ GraphKey make_key(const mm_sset* S, int dim, float alpha, float q, const mm_appr
     GraphKey k;
     memset(&k, 0, sizeof(k));
     (void)st;  // an executable graph may be launched into any stream
-    const void* ps[20] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
+    const void* ps[23] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
                           sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child, sb.jpart,
-                          sb.rord, sb.rpos, sb.tile_nu};
+                          sb.rord, sb.rpos, sb.tile_nu, sb.tperm, sb.tpos, sb.tile_box};
     memcpy(k.p, ps, sizeof(ps));
     k.v[0] = S->n;
     k.v[1] = S->nnz;
@@ -1615,7 +1663,7 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
                 return MM_ERR_INVALID_ARGUMENT;
             }
             MM_CU(cudaMemsetAsync(sbl.flags, 0, 4 * sizeof(int32_t), ls), "mm_layout memset");
-            if (app) MM_CU(prepare_approx(nf, app, sbl, ls), "mm_layout prepare_approx");
+            if (app) MM_CU(prepare_approx(nf, dim, app, cur, sbl, ls), "mm_layout prepare_approx");
             float* other = (cur == xa) ? xb : xa;
             const float* res = nullptr;
             int32_t nsw = 0;

@@ -80,14 +80,16 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 // repulsion partials of this vertex (static schedule slots), fetched
                 // first so that their latency overlaps the S-row loads
                 const int stride = DIM == 2 ? 2 : 4;
-                const int64_t tb = i / a.tpb;
+                // kernel (c) writes partials by target slot (spatial order, Q27)
+                const int64_t pi = a.tpos != nullptr ? (int64_t)__ldg(a.tpos + i) : i;
+                const int64_t tb = pi / a.tpb;
                 const int32_t nslot =
                     a.jpart ? sched_first_cta_tri(tri_prefix((int32_t)tb + 1, a.tri) - 1, a.tri) -
                                   sched_first_cta_tri(tri_prefix((int32_t)tb, a.tri), a.tri) + 1
                             : sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
                                   sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
                 for (int p = 0; p < nslot; ++p) {
-                    const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
+                    const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, pi);
                     R.x += v.x;
                     R.y += v.y;
                     R.z += v.z;

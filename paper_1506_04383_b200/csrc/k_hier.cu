@@ -351,20 +351,151 @@ __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const in
     rep_lo[slot] = make_float4((float)(mx - hx), (float)(my - hy), (float)(mz - hz), 0.f);
 }
 
-// Mass order of the representatives (Q26): nu(v) = member count
-__global__ void k_rep_mass(int32_t k, const int32_t* __restrict__ mptr, int32_t* __restrict__ nu) {
-    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-    if (v < k) nu[v] = mptr[v + 1] - mptr[v];
+// ---- orders for kernel (c) (Q26/Q27), computed once per level -----
+// float <-> order-preserving unsigned (for atomic min/max of a bounding box)
+__device__ __forceinline__ uint32_t f2ord(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
-// rpos = inverse of rord; tile_nu[t] = the common mass of slots [256 t, 256 t + 255] or 0
-__global__ void k_rep_slots(int32_t k, const int32_t* __restrict__ rord, const int32_t* __restrict__ nu_sorted,
+__device__ __forceinline__ float ord2f(uint32_t u) {
+    return __uint_as_float((u & 0x80000000u) ? (u & 0x7fffffffu) : ~u);
+}
+__global__ void k_box_init(uint32_t* box) {
+    if (threadIdx.x < 3) box[threadIdx.x] = 0xffffffffu;
+    else if (threadIdx.x < 6) box[threadIdx.x] = 0u;
+}
+template <int DIM>
+__global__ void k_bbox(int32_t n, const float* __restrict__ x, uint32_t* __restrict__ box) {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = load_x<DIM>(x, i);
+        const float v[3] = {p.x, p.y, p.z};
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            mn[c] = fminf(mn[c], v[c]);
+            mx[c] = fmaxf(mx[c], v[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        }
+        if ((threadIdx.x & 31) == 0 && mn[c] <= mx[c]) {  // min/max: order-independent, deterministic
+            atomicMin(box + c, f2ord(mn[c]));
+            atomicMax(box + 3 + c, f2ord(mx[c]));
+        }
+    }
+}
+__device__ __forceinline__ uint32_t spread2(uint32_t v) {  // 16 bits -> even bits
+    v &= 0xffffu;
+    v = (v | (v << 8)) & 0x00ff00ffu;
+    v = (v | (v << 4)) & 0x0f0f0f0fu;
+    v = (v | (v << 2)) & 0x33333333u;
+    v = (v | (v << 1)) & 0x55555555u;
+    return v;
+}
+__device__ __forceinline__ uint32_t spread3(uint32_t v) {  // 10 bits -> every third bit
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000ffu;
+    v = (v | (v << 8)) & 0x0300f00fu;
+    v = (v | (v << 4)) & 0x030c30c3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+// Morton (Z-order) key of p quantised to the box: 16 bits per axis (2-D), 10 (3-D)
+template <int DIM>
+__device__ __forceinline__ uint32_t morton_key(const float4& p, const uint32_t* box) {
+    const int B = DIM == 2 ? 16 : 10;
+    const float cells = (float)(1u << B);
+    const float v[3] = {p.x, p.y, p.z};
+    uint32_t q[3] = {0, 0, 0};
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+        const float lo = ord2f(box[c]), hi = ord2f(box[3 + c]);
+        const float ext = hi - lo;
+        float t = ext > 0.f ? (v[c] - lo) / ext * cells : 0.f;
+        t = fminf(fmaxf(t, 0.f), cells - 1.f);
+        q[c] = (uint32_t)t;  // NaN -> 0
+    }
+    return DIM == 2 ? (spread2(q[0]) | (spread2(q[1]) << 1))
+                    : (spread3(q[0]) | (spread3(q[1]) << 1) | (spread3(q[2]) << 2));
+}
+template <int DIM>
+__global__ void k_target_keys(int32_t n, const float* __restrict__ x, const uint32_t* __restrict__ box,
+                              uint32_t* __restrict__ key) {
+    const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) key[i] = morton_key<DIM>(load_x<DIM>(x, i), box);
+}
+// representative v: key = (nu(v) << 32) | Morton key of its first member
+// (nu = member count; the first member stands in for the centroid)
+template <int DIM>
+__global__ void k_rep_keys(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
+                           const float* __restrict__ x, const uint32_t* __restrict__ box, uint64_t* __restrict__ key) {
+    const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+    if (v >= k) return;
+    const int32_t b = mptr[v], e = mptr[v + 1];
+    const uint32_t mk = e > b ? morton_key<DIM>(load_x<DIM>(x, mem[b]), box) : 0u;
+    key[v] = ((uint64_t)(uint32_t)(e - b) << 32) | mk;
+}
+// rpos = inverse of rord; tile_nu[t] = the common mass of slots [tile t, tile t + tile - 1] or 0
+__global__ void k_rep_slots(int32_t k, const int32_t* __restrict__ rord, const uint64_t* __restrict__ key_sorted,
                             int32_t* __restrict__ rpos, int32_t* __restrict__ tile_nu, int tile) {
     const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= k) return;
     rpos[rord[s]] = s;
     if (s % tile == 0) {
         const int32_t last = min(s + tile - 1, k - 1);
-        tile_nu[s / tile] = nu_sorted[s] == nu_sorted[last] ? nu_sorted[s] : 0;
+        const uint32_t a = (uint32_t)(key_sorted[s] >> 32), b = (uint32_t)(key_sorted[last] >> 32);
+        tile_nu[s / tile] = a == b ? (int32_t)a : 0;
+    }
+}
+__global__ void k_scatter_inv(int32_t n, const int32_t* __restrict__ perm, int32_t* __restrict__ inv) {
+    const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s < n) inv[perm[s]] = s;
+}
+// per source tile of kernel (c): box of the representatives' hi coordinates
+// {min x, min y, min z, max |coordinate|}, {max x, max y, max z, 0}
+template <int DIM>
+__global__ void k_tile_box(int32_t k, const float4* __restrict__ rep_hi, float4* __restrict__ tile_box) {
+    const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    if (s < k) {
+        const float4 p = rep_hi[s];
+        mn[0] = mx[0] = p.x;
+        mn[1] = mx[1] = p.y;
+        if (DIM == 3) mn[2] = mx[2] = p.z;
+    }
+    __shared__ float red[8][6];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        }
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        for (int c = 0; c < 3; ++c) {
+            red[w][c] = mn[c];
+            red[w][3 + c] = mx[c];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int ww = 1; ww < (int)(blockDim.x >> 5); ++ww)
+            for (int c = 0; c < 3; ++c) {
+                red[0][c] = fminf(red[0][c], red[ww][c]);
+                red[0][3 + c] = fmaxf(red[0][3 + c], red[ww][3 + c]);
+            }
+        float X = 0.f;
+        for (int c = 0; c < DIM; ++c) X = fmaxf(X, fmaxf(fabsf(red[0][c]), fabsf(red[0][3 + c])));
+        if (DIM == 2) red[0][2] = red[0][5] = 0.f;
+        tile_box[2 * blockIdx.x] = make_float4(red[0][0], red[0][1], red[0][2], X);
+        tile_box[2 * blockIdx.x + 1] = make_float4(red[0][3], red[0][4], red[0][5], 0.f);
     }
 }
 
@@ -661,27 +792,52 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
     return cudaGetLastError();
 }
 
-cudaError_t rep_mass_order(int32_t k, const int32_t* mptr, int tile, int32_t* nu, int32_t* nu_sorted,
-                           const int32_t* iota, int32_t* rord, int32_t* rpos, int32_t* tile_nu, void* tmp,
-                           size_t tmp_bytes, cudaStream_t st) {
-    if (k <= 0) return cudaSuccess;
+cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
+                          int tile, const int32_t* iota, uint32_t* box, uint32_t* tkey, uint32_t* tkey_sorted,
+                          int32_t* tperm, int32_t* tpos, uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord,
+                          int32_t* rpos, int32_t* tile_nu, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+    if (k <= 0 || n <= 0) return cudaSuccess;
     {
-        LaunchScope ls("rep_mass", st);
-        k_rep_mass<<<nblk(k), 256, 0, st>>>(k, mptr, nu);
+        LaunchScope ls("order_keys", st);
+        k_box_init<<<1, 32, 0, st>>>(box);
+        const int nb = std::min(nblk(n), 4 * 148);
+        if (dim == 2) {
+            k_bbox<2><<<nb, 256, 0, st>>>(n, x, box);
+            k_target_keys<2><<<nblk(n), 256, 0, st>>>(n, x, box, tkey);
+            k_rep_keys<2><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, box, rkey);
+        } else {
+            k_bbox<3><<<nb, 256, 0, st>>>(n, x, box);
+            k_target_keys<3><<<nblk(n), 256, 0, st>>>(n, x, box, tkey);
+            k_rep_keys<3><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, box, rkey);
+        }
     }
+    cudaError_t e;
     {
-        LaunchScope ls("cub_sort_mass", st);
-        // stable: equal masses keep representative-id order
-        const cudaError_t e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, nu, nu_sorted, iota, rord, k, 0, 31, st);
+        LaunchScope ls("cub_sort_order", st);
+        // stable: equal keys keep id order
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, tkey, tkey_sorted, iota, tperm, n, 0, 32, st);
+        if (e != cudaSuccess) return e;
+        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, rkey, rkey_sorted, iota, rord, k, 0, 64, st);
         if (e != cudaSuccess) return e;
     }
-    LaunchScope ls("rep_slots", st);
-    k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, nu_sorted, rpos, tile_nu, tile);
+    LaunchScope ls("order_slots", st);
+    k_scatter_inv<<<nblk(n), 256, 0, st>>>(n, tperm, tpos);
+    k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, rkey_sorted, rpos, tile_nu, tile);
     return cudaGetLastError();
 }
 
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                            const int32_t* rord, float4* rep_hi, float4* rep_lo, cudaStream_t st) {
+                            const int32_t* rord, float4* rep_hi, float4* rep_lo, float4* tile_box, int tile,
+                            cudaStream_t st) {
+    if (tile_box != nullptr && k > 0) {
+        const cudaError_t e = launch_centroid(dim, n, k, mptr, mem, x, rord, rep_hi, rep_lo, nullptr, tile, st);
+        if (e != cudaSuccess) return e;
+        LaunchScope ls("tile_box", st);
+        const int nt = (k + tile - 1) / tile;
+        if (dim == 2) k_tile_box<2><<<nt, tile, 0, st>>>(k, rep_hi, tile_box);
+        else k_tile_box<3><<<nt, tile, 0, st>>>(k, rep_hi, tile_box);
+        return cudaGetLastError();
+    }
     LaunchScope ls("centroid", st);
     // lanes per representative: about 4 members per lane
     const double mean = k > 0 ? (double)n / k : 1.0;

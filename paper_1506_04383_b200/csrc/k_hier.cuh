@@ -33,15 +33,20 @@ cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr,
                          int32_t* key_sorted, int32_t* iota, int32_t* cnt, void* tmp, size_t tmp_bytes,
                          cudaStream_t st);
 cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int32_t* out, cudaStream_t st);
-// representatives in mass order (Q26): rord[slot] = rep id (stable by id), rpos = its
-// inverse, tile_nu[t] = common mass of slots [tile t, tile (t+1)) or 0; nu, nu_sorted: int32[k] scratch;
-// iota[0..k) = 0..k-1
-cudaError_t rep_mass_order(int32_t k, const int32_t* mptr, int tile, int32_t* nu, int32_t* nu_sorted,
-                           const int32_t* iota, int32_t* rord, int32_t* rpos, int32_t* tile_nu, void* tmp,
-                           size_t tmp_bytes, cudaStream_t st);
-// rord nullable: representative v at slot v; else rep rord[s] is written at slot s
+// Orders for kernel (c), once per level (Q26, Q27) from the positions x:
+//  targets: tperm[slot] = vertex id in Morton order of x (tpos = inverse);
+//  representatives: rord[slot] = rep id ordered by (mass nu, Morton key of the first
+//  member), rpos = inverse, tile_nu[t] = common mass of slots [tile t, tile (t+1)) or 0.
+// iota[0..max(n,k)) = 0, 1, ...; box: uint32[6] scratch; tkey*: uint32[n]; rkey*: uint64[k]
+cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
+                          int tile, const int32_t* iota, uint32_t* box, uint32_t* tkey, uint32_t* tkey_sorted,
+                          int32_t* tperm, int32_t* tpos, uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord,
+                          int32_t* rpos, int32_t* tile_nu, void* tmp, size_t tmp_bytes, cudaStream_t st);
+// rord nullable: representative v at slot v; else rep rord[s] is written at slot s.
+// tile_box nullable: else the box of every `tile` slots is written (kernel (c)'s skip test, Q27)
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                            const int32_t* rord, float4* rep_hi, float4* rep_lo, cudaStream_t st);
+                            const int32_t* rord, float4* rep_hi, float4* rep_lo, float4* tile_box, int tile,
+                            cudaStream_t st);
 cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
                            int32_t level, float* x, cudaStream_t st);
 cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,

@@ -37,6 +37,15 @@ namespace {
 
 constexpr int kBlock = 256;   // threads per CTA = sources per shared-memory tile
 static_assert(kBlock == kCoarseTile, "tile_nu granularity");
+#ifndef MM_T2
+#define MM_T2 4  // targets per thread, 2-D (experiments: tools/gvar builds)
+#endif
+#ifndef MM_T3
+#define MM_T3 2
+#endif
+#ifndef MM_REP_UNR
+#define MM_REP_UNR 4
+#endif
 
 // 1/|d|^(q+2) for a packed pair of r^2.  q = 0 batched: one MUFU for both,
 // 1/a = b * rcp(a*b), 1/b = a * rcp(a*b) (FMUL + MUFU + FMUL2 with swapped halves).
@@ -52,27 +61,31 @@ __device__ __forceinline__ f2x inv_pair(f2x r2, float cexp) {
     }
 }
 
-#ifndef MM_COARSE_MASK
-#define MM_COARSE_MASK 0  // 1: exclude H(i) inside kernel (c) (experiments; round-1 design)
+#ifndef MM_COARSE_BMASK_FAST
+#define MM_COARSE_BMASK_FAST 1  // batched reciprocals in these target groups of kernel (c)'s no-lo tiles
 #endif
+constexpr float kFarRel2 = 1.0f / 16384.f;  // Q27: a tile is far from a warp when sep^2 >= (2^-7 X)^2
 // One shared-memory source tile against the thread's T = 2G targets: T* += the
 // pair terms.  PAIR_NU: multiply every pair by its representative's mass nu
 // (coarse tiles of mixed mass); otherwise the caller scales the tile sum.
-template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, int UNR, bool PAIR_NU>
+// LO: difference against the representative as (x_i - hi) - lo (Q24); without it
+// (x_i - hi) only, for tiles far from every target of the warp (Q27).
+template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, int UNR, bool PAIR_NU, bool LO>
 __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const float4* sm_b, const f2x (&X)[G],
                                            const f2x (&Y)[G], const f2x (&Z)[G], f2x (&TX)[G], f2x (&TY)[G],
-                                           f2x (&TZ)[G], float cexp, const int32_t* hi, int64_t t0) {
+                                           f2x (&TZ)[G], float cexp) {
     const f2x eps2 = pk(kEps2, kEps2);
     const float2* sm2 = reinterpret_cast<const float2*>(sm_a);
-    (void)hi;
-    (void)t0;
 #pragma unroll UNR
     for (int jj = 0; jj < cnt; ++jj) {
         float sx, sy, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f, nu = 1.f;
         if constexpr (COARSE) {
-            const float4 a = sm_a[jj], b = sm_b[jj];
+            const float4 a = sm_a[jj];
             sx = a.x; sy = a.y; sz = a.z; nu = a.w;
-            lx = b.x; ly = b.y; lz = b.z;
+            if constexpr (LO) {
+                const float4 b = sm_b[jj];
+                lx = b.x; ly = b.y; lz = b.z;
+            }
         } else if constexpr (DIM == 2) {
             const float2 a = sm2[jj];
             sx = a.x; sy = a.y;
@@ -81,11 +94,12 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
             sx = a.x; sy = a.y; sz = a.z;
         }
         (void)nu;
+        (void)lx; (void)ly; (void)lz;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
             f2x dx = sub_bc(X[gg], sx);
             f2x dy = sub_bc(Y[gg], sy);
-            if constexpr (COARSE) {
+            if constexpr (COARSE && LO) {
                 dx = sub_bc(dx, lx);
                 dy = sub_bc(dy, ly);
             }
@@ -94,12 +108,12 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
             f2x dz = 0ull;
             if constexpr (DIM == 3) {
                 dz = sub_bc(Z[gg], sz);
-                if constexpr (COARSE) dz = sub_bc(dz, lz);
+                if constexpr (COARSE && LO) dz = sub_bc(dz, lz);
                 r2 = fma2(dz, dz, r2);
             }
             // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
             f2x inv;
-            if constexpr (PAIR_NU && !MM_COARSE_MASK) {
+            if constexpr (PAIR_NU) {
                 // all k representatives, the own one H(i) included: kernel (a)
                 // subtracts that term (Q25); nu folded into the
                 // batched reciprocal: nu/a = b * (nu * rcp(ab))
@@ -114,10 +128,6 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
             } else {
                 inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
             }
-            if constexpr (COARSE && MM_COARSE_MASK) {
-                const int32_t j = (int32_t)(t0 + jj);
-                inv = mul2(inv, pk(j == hi[2 * gg] ? 0.f : nu, j == hi[2 * gg + 1] ? 0.f : nu));
-            }
             TX[gg] = fma2(dx, inv, TX[gg]);
             TY[gg] = fma2(dy, inv, TY[gg]);
             if constexpr (DIM == 3) TZ[gg] = fma2(dz, inv, TZ[gg]);
@@ -128,22 +138,25 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
 template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4>
 __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
                                                     const float4* __restrict__ rep_hi,
-                                                    const float4* __restrict__ rep_lo,
-                                                    const int32_t* __restrict__ anc,
-                                                    const int32_t* __restrict__ tile_nu, float cexp, Sched sch,
-                                                    float* __restrict__ part) {
+                                                    const float4* __restrict__ rep_lo, CoarseOrder co, float cexp,
+                                                    Sched sch, float* __restrict__ part) {
     static_assert(T % 2 == 0, "targets are processed in packed pairs");
     constexpr int G = T / 2;
     constexpr int TPB = kBlock * T;
     constexpr int stride = DIM == 2 ? 2 : 4;
+    constexpr int kFastMask = (DIM == 2 && !QPOW) ? MM_COARSE_BMASK_FAST : 0;
     // shared source tile: exact 2-D -> float2; exact 3-D -> float4; coarse -> hi/lo float4 pairs
     __shared__ float4 sm_a[kBlock];
     __shared__ float4 sm_b[COARSE ? kBlock : 1];
     float2* sm2 = reinterpret_cast<float2*>(sm_a);
 
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t g = blockIdx.x;
     const int64_t u0 = (int64_t)g * sch.U / sch.G, u1 = (int64_t)(g + 1) * sch.U / sch.G;
+    // target slot of (group gg, half h): each warp owns 32 T consecutive slots
+    auto tslot = [&](int64_t base, int gg, int h) -> int64_t {
+        return base + (int64_t)warp * (32 * T) + (2 * gg + h) * 32 + lane;
+    };
 
     for (int64_t u = u0; u < u1;) {
         const int32_t tb = (int32_t)(u / sch.Ub);
@@ -151,27 +164,49 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
         const int32_t tile0 = (int32_t)(u - (int64_t)tb * sch.Ub), tile1 = (int32_t)(seg_end - (int64_t)tb * sch.Ub);
         // targets of this block (registers), packed pairwise
         f2x X[G], Y[G], Z[G], AX[G], AY[G], AZ[G];
-        int32_t hi[T];
         const int64_t base = (int64_t)tb * TPB;
+        float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
-            const int64_t ia = base + (2 * gg) * kBlock + tid, ib = base + (2 * gg + 1) * kBlock + tid;
-            const int64_t ca = ia < n_tgt ? ia : n_tgt - 1, cb = ib < n_tgt ? ib : n_tgt - 1;
+            const int64_t ia = tslot(base, gg, 0), ib = tslot(base, gg, 1);
+            int64_t ca = ia < n_tgt ? ia : n_tgt - 1, cb = ib < n_tgt ? ib : n_tgt - 1;
+            if (COARSE && co.tperm != nullptr) {
+                ca = __ldg(co.tperm + ca);
+                cb = __ldg(co.tperm + cb);
+            }
             // scalar loads, so that ptxas can place (x_a, x_b) in one aligned
             // register pair for the whole loop (vector loads would interleave
             // the halves and force MOVs to re-form the pair at every use)
             const float* pa = x + ca * stride;
             const float* pb = x + cb * stride;
-            X[gg] = pk(__ldg(pa), __ldg(pb));
-            Y[gg] = pk(__ldg(pa + 1), __ldg(pb + 1));
-            Z[gg] = (DIM == 3) ? pk(__ldg(pa + 2), __ldg(pb + 2)) : 0ull;
+            const float xa = __ldg(pa), xb = __ldg(pb), ya = __ldg(pa + 1), yb = __ldg(pb + 1);
+            const float za = DIM == 3 ? __ldg(pa + 2) : 0.f, zb = DIM == 3 ? __ldg(pb + 2) : 0.f;
+            X[gg] = pk(xa, xb);
+            Y[gg] = pk(ya, yb);
+            Z[gg] = (DIM == 3) ? pk(za, zb) : 0ull;
             AX[gg] = AY[gg] = AZ[gg] = 0ull;
-            if constexpr (COARSE && MM_COARSE_MASK) {
-                hi[2 * gg] = __ldg(anc + ca);
-                hi[2 * gg + 1] = __ldg(anc + cb);
+            if constexpr (COARSE) {
+                wlo[0] = fminf(wlo[0], fminf(xa, xb));
+                whi[0] = fmaxf(whi[0], fmaxf(xa, xb));
+                wlo[1] = fminf(wlo[1], fminf(ya, yb));
+                whi[1] = fmaxf(whi[1], fmaxf(ya, yb));
+                wlo[2] = fminf(wlo[2], fminf(za, zb));
+                whi[2] = fmaxf(whi[2], fmaxf(za, zb));
             }
         }
-        (void)hi;
+        // the warp's target box (Q27): lo-free tiles need every target of the warp far away
+        float wX = 0.f;
+        if constexpr (COARSE) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    wlo[c] = fminf(wlo[c], __shfl_xor_sync(0xffffffffu, wlo[c], o));
+                    whi[c] = fmaxf(whi[c], __shfl_xor_sync(0xffffffffu, whi[c], o));
+                }
+                wX = fmaxf(wX, fmaxf(fabsf(wlo[c]), fabsf(whi[c])));
+            }
+        }
         for (int32_t tile = tile0; tile < tile1; ++tile) {
             const int64_t t0 = (int64_t)tile * kBlock;
             const int cnt = (int)min((int64_t)kBlock, (int64_t)n_src - t0);
@@ -194,10 +229,25 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             // coarse tiles whose representatives all have the same mass nu
             // (representatives are stored in mass order, Q26) sum
             // (x_i - x')/|x_i - x'|^(q+2) and scale the tile sum by nu once
-            const int tnu = (COARSE && tile_nu != nullptr) ? __ldg(tile_nu + tile) : 0;
+            const int tnu = (COARSE && co.tile_nu != nullptr) ? __ldg(co.tile_nu + tile) : 0;
+            // far tile (Q27): every target of the warp is at least 2^-7 X from the
+            // tile's box, so dropping lo perturbs each pair term by < 2^-17 (q+1) relative
+            bool far = false;
+            if (COARSE && co.tile_box != nullptr) {
+                const float4 blo = __ldg(co.tile_box + 2 * tile), bhi = __ldg(co.tile_box + 2 * tile + 1);
+                const float sx = fmaxf(0.f, fmaxf(blo.x - whi[0], wlo[0] - bhi.x));
+                const float sy = fmaxf(0.f, fmaxf(blo.y - whi[1], wlo[1] - bhi.y));
+                const float sz = fmaxf(0.f, fmaxf(blo.z - whi[2], wlo[2] - bhi.z));
+                const float XX = fmaxf(wX, blo.w);
+                far = sx * sx + sy * sy + sz * sz >= XX * XX * kFarRel2;
+            }
             if (tnu > 0) {
-                tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, false>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp, hi,
-                                                                   t0);
+                if (far)
+                    tile_pairs<DIM, QPOW, COARSE, G, kFastMask, UNR, false, false>(cnt, sm_a, sm_b, X, Y, Z, TX, TY,
+                                                                                 TZ, cexp);
+                else
+                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, false, COARSE>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
+                                                                               cexp);
                 const f2x nu2 = pk((float)tnu, (float)tnu);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
@@ -206,8 +256,12 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
                     if constexpr (DIM == 3) AZ[gg] = fma2(TZ[gg], nu2, AZ[gg]);
                 }
             } else {
-                tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp, hi,
-                                                                    t0);
+                if (far)
+                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE, false>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
+                                                                               cexp);
+                else
+                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE, COARSE>(cnt, sm_a, sm_b, X, Y, Z, TX, TY,
+                                                                                TZ, cexp);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
                     AX[gg] = add2(AX[gg], TX[gg]);
@@ -221,7 +275,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
         float* out = part + (int64_t)slot * n_tgt * stride;
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
-            const int64_t ia = base + (2 * gg) * kBlock + tid, ib = base + (2 * gg + 1) * kBlock + tid;
+            const int64_t ia = tslot(base, gg, 0), ib = tslot(base, gg, 1);
             float ax0, ax1, ay0, ay1, az0 = 0.f, az1 = 0.f;
             upk(AX[gg], ax0, ax1);
             upk(AY[gg], ay0, ay1);
@@ -658,7 +712,7 @@ template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
     static const int occ = [] {  // per instantiation; queried once
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>, 1, MM_REP_UNR>,
                                                       kBlock, 0);
         return o > 0 ? o : 1;
     }();
@@ -677,7 +731,7 @@ int sm_count() {
     return sms;
 }
 
-int targets_per_thread(int dim) { return dim == 2 ? 4 : 2; }
+int targets_per_thread(int dim) { return dim == 2 ? MM_T2 : MM_T3; }
 
 }  // namespace
 
@@ -693,11 +747,11 @@ RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, boo
     s.U = (int64_t)s.TB * s.Ub;
     int occ;
     if (dim == 2) {
-        occ = coarse ? (qpow ? resident_ctas<2, true, true, 4>() : resident_ctas<2, false, true, 4>())
-                     : (qpow ? resident_ctas<2, true, false, 4>() : resident_ctas<2, false, false, 4>());
+        occ = coarse ? (qpow ? resident_ctas<2, true, true, MM_T2>() : resident_ctas<2, false, true, MM_T2>())
+                     : (qpow ? resident_ctas<2, true, false, MM_T2>() : resident_ctas<2, false, false, MM_T2>());
     } else {
-        occ = coarse ? (qpow ? resident_ctas<3, true, true, 2>() : resident_ctas<3, false, true, 2>())
-                     : (qpow ? resident_ctas<3, true, false, 2>() : resident_ctas<3, false, false, 2>());
+        occ = coarse ? (qpow ? resident_ctas<3, true, true, MM_T3>() : resident_ctas<3, false, true, MM_T3>())
+                     : (qpow ? resident_ctas<3, true, false, MM_T3>() : resident_ctas<3, false, false, MM_T3>());
     }
     s.G = (int32_t)std::max<int64_t>(1, std::min<int64_t>((int64_t)sm_count() * occ, s.U));
     // slots: max over target blocks of (CTAs touching the block)
@@ -712,26 +766,25 @@ RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, boo
 }
 
 cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_tgt, const float* x,
-                           int32_t n_src, const float4* rep_hi, const float4* rep_lo, const int32_t* anc,
-                           const int32_t* tile_nu, const RepulsePlan& p, float* part, cudaStream_t st) {
+                           int32_t n_src, const float4* rep_hi, const float4* rep_lo, const CoarseOrder& co,
+                           const RepulsePlan& p, float* part, cudaStream_t st) {
     const float cexp = -(q + 2.0f) * 0.5f;
     LaunchScope ls(coarse ? "repulse_coarse" : "repulse_exact", st);
 // batched reciprocals (BMASK) in half of the target groups for 2-D q = 0
 // (exact and coarse: measured faster by tools/ubench_repulse.cu); none for q > 0.
 #define MM_LAUNCH(D, Q, C, T) \
-    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, anc, \
-                                                                          MM_COARSE_MASK ? nullptr : tile_nu, cexp,  \
+    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>, 1, MM_REP_UNR><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, co, cexp,  \
                                                                           p.sch, part)
     if (dim == 2) {
-        if (!qpow && !coarse) MM_LAUNCH(2, false, false, 4);
-        else if (!qpow && coarse) MM_LAUNCH(2, false, true, 4);
-        else if (qpow && !coarse) MM_LAUNCH(2, true, false, 4);
-        else MM_LAUNCH(2, true, true, 4);
+        if (!qpow && !coarse) MM_LAUNCH(2, false, false, MM_T2);
+        else if (!qpow && coarse) MM_LAUNCH(2, false, true, MM_T2);
+        else if (qpow && !coarse) MM_LAUNCH(2, true, false, MM_T2);
+        else MM_LAUNCH(2, true, true, MM_T2);
     } else {
-        if (!qpow && !coarse) MM_LAUNCH(3, false, false, 2);
-        else if (!qpow && coarse) MM_LAUNCH(3, false, true, 2);
-        else if (qpow && !coarse) MM_LAUNCH(3, true, false, 2);
-        else MM_LAUNCH(3, true, true, 2);
+        if (!qpow && !coarse) MM_LAUNCH(3, false, false, MM_T3);
+        else if (!qpow && coarse) MM_LAUNCH(3, false, true, MM_T3);
+        else if (qpow && !coarse) MM_LAUNCH(3, true, false, MM_T3);
+        else MM_LAUNCH(3, true, true, MM_T3);
     }
 #undef MM_LAUNCH
     return cudaGetLastError();
@@ -739,7 +792,6 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
 
 int repulse_targets_per_block(int dim) { return kBlock * targets_per_thread(dim); }
 
-bool coarse_excludes_own() { return MM_COARSE_MASK != 0; }
 
 namespace {
 template <int DIM, bool QPOW>

@@ -52,12 +52,16 @@ struct EntropyPlan {
     int nblocks = 1;   // CTAs = FP64 partials
 };
 
+// Orders / metadata of kernel (c) (all nullable; Q26, Q27)
+struct CoarseOrder {
+    const int32_t* tperm = nullptr;    // target slot -> vertex id (spatial order); partials are written by slot
+    const int32_t* tile_nu = nullptr;  // [ceil(k/256)] common mass nu of a source tile, or 0 (mixed)
+    const float4* tile_box = nullptr;  // [2 ceil(k/256)] box of a tile's hi coordinates (.w of [0]: max |coord|)
+};
 RepulsePlan plan_repulse(int32_t n_tgt, int32_t n_src, int dim, bool coarse, bool qpow);
 int repulse_targets_per_block(int dim);
-bool coarse_excludes_own();  // kernel (c) built with MM_COARSE_MASK = 1
 cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_tgt, const float* x,
-                           int32_t n_src, const float4* rep_hi, const float4* rep_lo, const int32_t* anc,
-                           const int32_t* tile_nu /* nullable: [ceil(n_src/256)] mass of a uniform-mass tile, else 0 */,
+                           int32_t n_src, const float4* rep_hi, const float4* rep_lo, const CoarseOrder& co,
                            const RepulsePlan& p, float* part, cudaStream_t st);
 // sources per tile of the coarse kernel (granularity of tile_nu)
 constexpr int kCoarseTile = 256;
@@ -84,10 +88,10 @@ struct GatherArgs {
     const float* jpart = nullptr;  // nullable: rectangular schedule
     TriSched tri;
     // Eq.(3) own-representative term, subtracted because kernel (c) sums over
-    // all k representatives (nullable: exact mode, or kernel (c) built with
-    // MM_COARSE_MASK = 1)
+    // all k representatives (nullable: exact mode)
     const int32_t* anc = nullptr;
     const int32_t* rpos = nullptr;  // nullable: slot of representative v in rep_hi/rep_lo (mass order)
+    const int32_t* tpos = nullptr;  // nullable: slot of vertex i in kernel (c)'s partials (spatial order)
     const float4* rep_hi = nullptr;
     const float4* rep_lo = nullptr;
     // Eq.(3) sibling term (nullable: exact mode)

@@ -315,3 +315,24 @@ def test_exact_sweep_3d_symmetric_sampled(mm, n, q):
     rows = sample_rows(n, 1024, seed=11)
     want = oracle.sweep_exact(S, x.astype(np.float64), 0.05, q, rows=rows)
     assert_sweep_parity(got[rows], want, f"3-D n={n} q={q}")
+
+
+@pytest.mark.parametrize("offset", [0.0, 2.0e4])
+def test_approx_far_tiles_structured_layout(mm, offset):
+    """Eq.(3) on a layout with spatially compact clusters (the mesh drawn on its
+    grid, jittered), so most (warp, tile) pairs take kernel (c)'s lo-free far
+    path (Q27); translated by `offset` the threshold 2^-7 X grows and
+    more tiles keep hi/lo.  All rows against the oracle."""
+    w = workload("cfg3_mesh128")
+    lv = oracle_hierarchy("cfg3_mesh128")
+    anc = oracle.ancestor(lv, 0, 2)
+    k = lv[2].n
+    side = int(round(math.sqrt(w.n)))
+    ids = np.arange(w.n)
+    rng = np.random.default_rng(5)
+    x = np.stack([ids % side, ids // side], axis=1).astype(np.float64)
+    x += rng.uniform(-0.2, 0.2, size=x.shape) + offset
+    x = x.astype(np.float32)
+    got = _gpu_sweep(mm, w.S, x, w.alpha, w.q, lv[0].parent, anc, k)
+    want = oracle.sweep_approx(w.S, x.astype(np.float64), w.alpha, w.q, lv[0].parent, anc, k)
+    assert_sweep_parity(got, want, f"structured offset={offset}")
