@@ -229,6 +229,7 @@ struct SweepBufs {
     float4* tile_box = nullptr;  // [2 ceil(k / kCoarseTile)] per-tile box of the representatives
     uint64_t* rkey = nullptr;    // [2k] representative sort keys (scratch)
     uint32_t* box = nullptr;     // [8] layout box (scratch)
+    float4* frame = nullptr;     // [1] kernel (c)'s frame origin (Q28)
     bool reorder = false;        // recompute kernel (c)'s orders before every sweep
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -284,7 +285,7 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
         b += al((size_t)(n + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)n * 4) * 2 + al((size_t)(std::max(n, k) + 2) * 4);
         b += 2 * al((size_t)k * 4) + al((size_t)(k / kCoarseTile + 1) * 4);
-        b += 2 * al((size_t)n * 4) + al((size_t)(k / kCoarseTile + 1) * 32) + al((size_t)k * 16) + al(32);
+        b += 2 * al((size_t)n * 4) + al((size_t)(k / kCoarseTile + 1) * 32) + al((size_t)k * 16) + al(32) + al(16);
         b += al(cub_tmp_bytes(n));
     }
     return b + 4096;
@@ -316,6 +317,7 @@ bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double 
         sb.tile_box = cv.take<float4>((size_t)2 * (k / kCoarseTile + 1));
         sb.rkey = cv.take<uint64_t>((size_t)2 * k);
         sb.box = cv.take<uint32_t>(8);
+        sb.frame = cv.take<float4>(1);
         sb.tmp_bytes = cub_tmp_bytes(n);
         sb.tmp = cv.take<char>(sb.tmp_bytes);
     }
@@ -338,8 +340,9 @@ bool far_tiles() {
 // iota = 0..n-1 (k <= n); cnt / key_sorted are free scratch after prepare_approx.
 cudaError_t coarse_orders(int32_t n, int dim, const mm_approx* ap, const float* x, const SweepBufs& sb,
                           cudaStream_t st) {
-    return approx_orders(dim, n, ap->k, sb.mptr, sb.mem, x, kCoarseTile, sb.iota, sb.box,
-                         reinterpret_cast<uint32_t*>(sb.cnt), reinterpret_cast<uint32_t*>(sb.key_sorted), sb.tperm,
+    return approx_orders(dim, n, ap->k, sb.mptr, sb.mem, x, kCoarseTile, sb.iota, sb.box, sb.frame, sb.rep_hi,
+                         sb.rep_lo, reinterpret_cast<uint32_t*>(sb.cnt), reinterpret_cast<uint32_t*>(sb.key_sorted),
+                         sb.tperm,
                          sb.tpos, sb.rkey, sb.rkey + ap->k, sb.rord, sb.rpos, sb.tile_nu, sb.tmp, sb.tmp_bytes, st);
 }
 
@@ -375,11 +378,10 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     RepulsePlan p;
     SymPlan sp;
     if (ap) {
-        if (sb.reorder) {
-            e = coarse_orders(n, dim, ap, x_in, sb, st);
-            if (e != cudaSuccess) return e;
-        }
-        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, sb.rep_hi, sb.rep_lo,
+        // frame origin of this sweep's positions (Q28); with per-sweep orders it comes with them
+        e = sb.reorder ? coarse_orders(n, dim, ap, x_in, sb, st) : launch_frame(dim, n, x_in, sb.box, sb.frame, st);
+        if (e != cudaSuccess) return e;
+        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, sb.frame, sb.rep_hi, sb.rep_lo,
                             far_tiles() ? sb.tile_box : nullptr, kCoarseTile, st);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
@@ -387,6 +389,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         co.tperm = sb.tperm;
         co.tile_nu = sb.tile_nu;
         co.tile_box = far_tiles() ? sb.tile_box : nullptr;
+        co.frame = sb.frame;
         e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, co, p, sb.part, st);
     } else if (sb.jpart) {
         sp = plan_repulse_sym(n, dim);
@@ -419,6 +422,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         ga.anc = ap->ancestor;
         ga.rpos = sb.rpos;
         ga.tpos = sb.tpos;
+        ga.frame = sb.frame;
         ga.rep_hi = sb.rep_hi;
         ga.rep_lo = sb.rep_lo;
     }
@@ -1020,7 +1024,7 @@ bool graphs_enabled() {
 // captured launches depend on (pointers, sizes, parameters).  A hit relaunches
 // the executable graph; capture + instantiate is paid once per distinct key.
 struct GraphKey {
-    const void* p[23];
+    const void* p[24];
     int64_t v[8];
     float f[2];
     int32_t kind = 0;      // 0: K fixed sweeps; 1: device-driven schedule loop of one level
@@ -1072,9 +1076,9 @@ GraphKey make_key(const mm_sset* S, int dim, float alpha, float q, const mm_appr
     GraphKey k;
     memset(&k, 0, sizeof(k));
     (void)st;  // an executable graph may be launched into any stream
-    const void* ps[23] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
+    const void* ps[24] = {S->row_ptr, S->col, S->d, S->w, src, bufA, bufB, stats, sb.part, sb.stat_partial,
                           sb.flags, sb.rep_hi, sb.rep_lo, sb.mptr, ap ? ap->ancestor : nullptr, sb.child, sb.jpart,
-                          sb.rord, sb.rpos, sb.tile_nu, sb.tperm, sb.tpos, sb.tile_box};
+                          sb.rord, sb.rpos, sb.tile_nu, sb.tperm, sb.tpos, sb.tile_box, sb.frame};
     memcpy(k.p, ps, sizeof(ps));
     k.v[0] = S->n;
     k.v[1] = S->nnz;

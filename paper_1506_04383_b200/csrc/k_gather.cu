@@ -147,12 +147,13 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 int32_t h = __ldg(a.anc + i);
                 if (a.rpos != nullptr) h = __ldg(a.rpos + h);
                 const float4 rh = __ldg(a.rep_hi + h), rl = __ldg(a.rep_lo + h);
-                const float dx = (xi.x - rh.x) - rl.x, dy = (xi.y - rh.y) - rl.y;
+                const float4 fr = a.frame != nullptr ? __ldg(a.frame) : make_float4(0.f, 0.f, 0.f, 0.f);
+                const float dx = ((xi.x - fr.x) - rh.x) - rl.x, dy = ((xi.y - fr.y) - rh.y) - rl.y;
                 float r2 = fmaf(dx, dx, kEps2);
                 r2 = fmaf(dy, dy, r2);
                 float dz = 0.f;
                 if constexpr (DIM == 3) {
-                    dz = (xi.z - rh.z) - rl.z;
+                    dz = ((xi.z - fr.z) - rh.z) - rl.z;
                     r2 = fmaf(dz, dz, r2);
                 }
                 const float inv = inv_pow<QPOW>(r2, cexp) * rh.w;

@@ -320,7 +320,8 @@ __global__ void k_compose(int32_t n, const int32_t* __restrict__ a, const int32_
 template <int DIM, int G>
 __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
                            const float* __restrict__ x, const int32_t* __restrict__ rord,
-                           float4* __restrict__ rep_hi, float4* __restrict__ rep_lo) {
+                           const float4* __restrict__ frame, float4* __restrict__ rep_hi,
+                           float4* __restrict__ rep_lo) {
     const int64_t tg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int32_t slot = (int32_t)(tg / G);
     const int32_t v = (rord != nullptr && slot < k) ? __ldg(rord + slot) : slot;
@@ -345,7 +346,9 @@ __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const in
     }
     if (slot >= k || lg != 0) return;
     const double nu = (double)(e - b);
-    const double mx = sx / nu, my = sy / nu, mz = DIM == 3 ? sz / nu : 0.0;
+    // relative to the frame origin (Q28; exact FP64 subtraction of an FP32 value)
+    const float4 f = frame != nullptr ? *frame : make_float4(0.f, 0.f, 0.f, 0.f);
+    const double mx = sx / nu - (double)f.x, my = sy / nu - (double)f.y, mz = DIM == 3 ? sz / nu - (double)f.z : 0.0;
     const float hx = (float)mx, hy = (float)my, hz = (float)mz;
     rep_hi[slot] = make_float4(hx, hy, hz, (float)nu);
     rep_lo[slot] = make_float4((float)(mx - hx), (float)(my - hy), (float)(mz - hz), 0.f);
@@ -389,6 +392,22 @@ __global__ void k_bbox(int32_t n, const float* __restrict__ x, uint32_t* __restr
         }
     }
 }
+// Frame origin c (Q28): per axis, a float c with c/2 <= x <= 2c (or 2c <= x <= c/2)
+// for every coordinate of the box, so that x - c is exact in FP32 (Sterbenz);
+// 0 when no such c exists (a box that reaches 0 or spans a factor > 3)
+template <int DIM>
+__global__ void k_frame(const uint32_t* __restrict__ box, float4* __restrict__ frame) {
+    if (threadIdx.x != 0) return;
+    float c[3] = {0.f, 0.f, 0.f};
+    for (int a = 0; a < DIM; ++a) {
+        const float lo = ord2f(box[a]), hi = ord2f(box[3 + a]);
+        if (!(lo <= hi)) continue;  // empty or non-finite box
+        const float m = 0.5f * lo + 0.5f * hi;
+        const bool ok = (lo > 0.f && 0.5f * m <= lo && hi <= 2.0f * m) || (hi < 0.f && 0.5f * m >= hi && lo >= 2.0f * m);
+        c[a] = ok ? m : 0.f;
+    }
+    *frame = make_float4(c[0], c[1], c[2], 0.f);
+}
 __device__ __forceinline__ uint32_t spread2(uint32_t v) {  // 16 bits -> even bits
     v &= 0xffffu;
     v = (v | (v << 8)) & 0x00ff00ffu;
@@ -429,16 +448,16 @@ __global__ void k_target_keys(int32_t n, const float* __restrict__ x, const uint
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) key[i] = morton_key<DIM>(load_x<DIM>(x, i), box);
 }
-// representative v: key = (nu(v) << 32) | Morton key of its first member
-// (nu = member count; the first member stands in for the centroid)
+// representative keys from its (frame-relative) centroid
 template <int DIM>
-__global__ void k_rep_keys(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
-                           const float* __restrict__ x, const uint32_t* __restrict__ box, uint64_t* __restrict__ key) {
+__global__ void k_rep_keys_c(int32_t k, const int32_t* __restrict__ mptr, const float4* __restrict__ rep_hi,
+                             const float4* __restrict__ frame, const uint32_t* __restrict__ box,
+                             uint64_t* __restrict__ key) {
     const int32_t v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= k) return;
-    const int32_t b = mptr[v], e = mptr[v + 1];
-    const uint32_t mk = e > b ? morton_key<DIM>(load_x<DIM>(x, mem[b]), box) : 0u;
-    key[v] = ((uint64_t)(uint32_t)(e - b) << 32) | mk;
+    const float4 f = *frame, h = rep_hi[v];
+    const float4 p = make_float4(h.x + f.x, h.y + f.y, h.z + f.z, 0.f);
+    key[v] = ((uint64_t)(uint32_t)(mptr[v + 1] - mptr[v]) << 32) | morton_key<DIM>(p, box);
 }
 // rpos = inverse of rord; tile_nu[t] = the common mass of slots [tile t, tile t + tile - 1] or 0
 __global__ void k_rep_slots(int32_t k, const int32_t* __restrict__ rord, const uint64_t* __restrict__ key_sorted,
@@ -792,26 +811,41 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
     return cudaGetLastError();
 }
 
+cudaError_t launch_frame(int dim, int32_t n, const float* x, uint32_t* box, float4* frame, cudaStream_t st) {
+    LaunchScope ls("frame", st);
+    k_box_init<<<1, 32, 0, st>>>(box);
+    const int nb = std::max(1, std::min(nblk(n), 4 * 148));
+    if (dim == 2) {
+        k_bbox<2><<<nb, 256, 0, st>>>(n, x, box);
+        k_frame<2><<<1, 32, 0, st>>>(box, frame);
+    } else {
+        k_bbox<3><<<nb, 256, 0, st>>>(n, x, box);
+        k_frame<3><<<1, 32, 0, st>>>(box, frame);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                          int tile, const int32_t* iota, uint32_t* box, uint32_t* tkey, uint32_t* tkey_sorted,
-                          int32_t* tperm, int32_t* tpos, uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord,
-                          int32_t* rpos, int32_t* tile_nu, void* tmp, size_t tmp_bytes, cudaStream_t st) {
+                          int tile, const int32_t* iota, uint32_t* box, float4* frame, float4* rep_hi,
+                          float4* rep_lo, uint32_t* tkey, uint32_t* tkey_sorted, int32_t* tperm, int32_t* tpos,
+                          uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord, int32_t* rpos, int32_t* tile_nu,
+                          void* tmp, size_t tmp_bytes, cudaStream_t st) {
     if (k <= 0 || n <= 0) return cudaSuccess;
+    cudaError_t e = launch_frame(dim, n, x, box, frame, st);
+    if (e != cudaSuccess) return e;
+    // centroids by representative id (the sort keys); the sweep rewrites them by slot
+    e = launch_centroid(dim, n, k, mptr, mem, x, nullptr, frame, rep_hi, rep_lo, nullptr, tile, st);
+    if (e != cudaSuccess) return e;
     {
         LaunchScope ls("order_keys", st);
-        k_box_init<<<1, 32, 0, st>>>(box);
-        const int nb = std::min(nblk(n), 4 * 148);
         if (dim == 2) {
-            k_bbox<2><<<nb, 256, 0, st>>>(n, x, box);
             k_target_keys<2><<<nblk(n), 256, 0, st>>>(n, x, box, tkey);
-            k_rep_keys<2><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, box, rkey);
+            k_rep_keys_c<2><<<nblk(k), 256, 0, st>>>(k, mptr, rep_hi, frame, box, rkey);
         } else {
-            k_bbox<3><<<nb, 256, 0, st>>>(n, x, box);
             k_target_keys<3><<<nblk(n), 256, 0, st>>>(n, x, box, tkey);
-            k_rep_keys<3><<<nblk(k), 256, 0, st>>>(k, mptr, mem, x, box, rkey);
+            k_rep_keys_c<3><<<nblk(k), 256, 0, st>>>(k, mptr, rep_hi, frame, box, rkey);
         }
     }
-    cudaError_t e;
     {
         LaunchScope ls("cub_sort_order", st);
         // stable: equal keys keep id order
@@ -827,10 +861,11 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
 }
 
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                            const int32_t* rord, float4* rep_hi, float4* rep_lo, float4* tile_box, int tile,
-                            cudaStream_t st) {
+                            const int32_t* rord, const float4* frame, float4* rep_hi, float4* rep_lo,
+                            float4* tile_box, int tile, cudaStream_t st) {
     if (tile_box != nullptr && k > 0) {
-        const cudaError_t e = launch_centroid(dim, n, k, mptr, mem, x, rord, rep_hi, rep_lo, nullptr, tile, st);
+        const cudaError_t e = launch_centroid(dim, n, k, mptr, mem, x, rord, frame, rep_hi, rep_lo, nullptr, tile,
+                                              st);
         if (e != cudaSuccess) return e;
         LaunchScope ls("tile_box", st);
         const int nt = (k + tile - 1) / tile;
@@ -846,12 +881,12 @@ cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, 
     const int nb = nblk((int64_t)k * G);
 #define MM_C(D)                                                                               \
     switch (G) {                                                                              \
-        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
-        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
-        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
-        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break;   \
-        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break; \
-        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, rep_hi, rep_lo); break; \
+        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
+        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
+        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
+        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
+        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break; \
+        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break; \
     }
     if (dim == 2) { MM_C(2) } else { MM_C(3) }
 #undef MM_C

@@ -33,20 +33,26 @@ cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr,
                          int32_t* key_sorted, int32_t* iota, int32_t* cnt, void* tmp, size_t tmp_bytes,
                          cudaStream_t st);
 cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int32_t* out, cudaStream_t st);
-// Orders for kernel (c), once per level (Q26, Q27) from the positions x:
+// Frame origin of kernel (c) (Q28): box = bounding box of x (uint32[6]
+// order-preserving scratch); frame->xyz = per-axis origin c with x - c exact in FP32, or 0
+cudaError_t launch_frame(int dim, int32_t n, const float* x, uint32_t* box, float4* frame, cudaStream_t st);
+// Orders for kernel (c) (Q26, Q27) from the positions x (also computes the frame):
 //  targets: tperm[slot] = vertex id in Morton order of x (tpos = inverse);
-//  representatives: rord[slot] = rep id ordered by (mass nu, Morton key of the first
-//  member), rpos = inverse, tile_nu[t] = common mass of slots [tile t, tile (t+1)) or 0.
-// iota[0..max(n,k)) = 0, 1, ...; box: uint32[6] scratch; tkey*: uint32[n]; rkey*: uint64[k]
+//  representatives: rord[slot] = rep id ordered by (mass nu, Morton key of its centroid),
+//  rpos = inverse, tile_nu[t] = common mass of slots [tile t, tile (t+1)) or 0.
+// rep_hi/rep_lo are overwritten (centroids by id, used as keys).
+// iota[0..max(n,k)) = 0, 1, ...; tkey*: uint32[n]; rkey*: uint64[k]
 cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                          int tile, const int32_t* iota, uint32_t* box, uint32_t* tkey, uint32_t* tkey_sorted,
-                          int32_t* tperm, int32_t* tpos, uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord,
-                          int32_t* rpos, int32_t* tile_nu, void* tmp, size_t tmp_bytes, cudaStream_t st);
+                          int tile, const int32_t* iota, uint32_t* box, float4* frame, float4* rep_hi,
+                          float4* rep_lo, uint32_t* tkey, uint32_t* tkey_sorted, int32_t* tperm, int32_t* tpos,
+                          uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord, int32_t* rpos, int32_t* tile_nu,
+                          void* tmp, size_t tmp_bytes, cudaStream_t st);
 // rord nullable: representative v at slot v; else rep rord[s] is written at slot s.
+// frame nullable: coordinates relative to the origin *frame (Q28).
 // tile_box nullable: else the box of every `tile` slots is written (kernel (c)'s skip test, Q27)
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
-                            const int32_t* rord, float4* rep_hi, float4* rep_lo, float4* tile_box, int tile,
-                            cudaStream_t st);
+                            const int32_t* rord, const float4* frame, float4* rep_hi, float4* rep_lo,
+                            float4* tile_box, int tile, cudaStream_t st);
 cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
                            int32_t level, float* x, cudaStream_t st);
 cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,

@@ -65,74 +65,134 @@ __device__ __forceinline__ f2x inv_pair(f2x r2, float cexp) {
 #define MM_COARSE_BMASK_FAST 1  // batched reciprocals in these target groups of kernel (c)'s no-lo tiles
 #endif
 constexpr float kFarRel2 = 1.0f / 16384.f;  // Q27: a tile is far from a warp when sep^2 >= (2^-7 X)^2
-// One shared-memory source tile against the thread's T = 2G targets: T* += the
-// pair terms.  PAIR_NU: multiply every pair by its representative's mass nu
-// (coarse tiles of mixed mass); otherwise the caller scales the tile sum.
-// LO: difference against the representative as (x_i - hi) - lo (Q24); without it
-// (x_i - hi) only, for tiles far from every target of the warp (Q27).
+// 2^y for a packed pair on the FMA and ALU pipes (no MUFU): y = n + f with n the
+// nearest integer (round-to-nearest through the 1.5 * 2^23 shifter), 2^f by a
+// degree-5 relative-error fit on [-1/2, 1/2] (max error 2.2e-7 in FP32, about
+// the 2 ulp of ex2.approx), 2^n added to the exponent field.  y is clamped to
+// [-125, 126] (below, ex2.approx.ftz would flush to 0; the difference is < 2^-125).
+__device__ __forceinline__ f2x ex2_poly2(f2x y) {
+    constexpr float kShift = 12582912.0f;
+    float y0, y1;
+    upk(y, y0, y1);
+    y0 = fminf(fmaxf(y0, -125.f), kExpClamp);
+    y1 = fminf(fmaxf(y1, -125.f), kExpClamp);
+    const f2x yc = pk(y0, y1);
+    const f2x t = add2(yc, pk(kShift, kShift));
+    float t0, t1;
+    upk(t, t0, t1);
+    const f2x tm = add2(t, pk(-kShift, -kShift));
+    const f2x f = fma2(tm, pk(-1.f, -1.f), yc);
+    f2x p = pk(0.0013266970636323094f, 0.0013266970636323094f);
+    p = fma2(p, f, pk(0.009675459936261177f, 0.009675459936261177f));
+    p = fma2(p, f, pk(0.05550742521882057f, 0.05550742521882057f));
+    p = fma2(p, f, pk(0.24022121727466583f, 0.24022121727466583f));
+    p = fma2(p, f, pk(0.6931469440460205f, 0.6931469440460205f));
+    p = fma2(p, f, pk(1.0000001192092896f, 1.0000001192092896f));
+    float p0, p1;
+    upk(p, p0, p1);
+    const int n0 = __float_as_int(t0) - 0x4B400000, n1 = __float_as_int(t1) - 0x4B400000;
+    return pk(__int_as_float(__float_as_int(p0) + (n0 << 23)), __int_as_float(__float_as_int(p1) + (n1 << 23)));
+}
+
+#ifndef MM_POLY_MASK3
+#define MM_POLY_MASK3 0x11  // 3-D q > 0: sources 0 and 4 of every 8 take the polynomial 2^y (Q29; measured best of 0x11, 0x25, 0x49, 0x55)
+#endif
+#ifndef MM_POLY_MASK2
+#define MM_POLY_MASK2 0x11  // 2-D q > 0
+#endif
+
+// One source (shared-memory slot jj) against the thread's T = 2G targets:
+// T* += the pair terms.  PAIR_NU: multiply every pair by its representative's
+// mass nu (coarse tiles of mixed mass); otherwise the caller scales the tile
+// sum.  LO: difference against the representative as (x_i - hi) - lo (Q24);
+// without it (x_i - hi) only, for tiles far from every target of the warp
+// (Q27).  POLY (q > 0): 2^y by ex2_poly2 instead of MUFU.EX2 (Q29).
+template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, bool PAIR_NU, bool LO, bool POLY>
+__device__ __forceinline__ void source_pairs(int jj, const float4* sm_a, const float4* sm_b, const f2x (&X)[G],
+                                             const f2x (&Y)[G], const f2x (&Z)[G], f2x (&TX)[G], f2x (&TY)[G],
+                                             f2x (&TZ)[G], float cexp) {
+    const f2x eps2 = pk(kEps2, kEps2);
+    const float2* sm2 = reinterpret_cast<const float2*>(sm_a);
+    float sx, sy, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f, nu = 1.f;
+    if constexpr (COARSE) {
+        const float4 a = sm_a[jj];
+        sx = a.x; sy = a.y; sz = a.z; nu = a.w;
+        if constexpr (LO) {
+            const float4 b = sm_b[jj];
+            lx = b.x; ly = b.y; lz = b.z;
+        }
+    } else if constexpr (DIM == 2) {
+        const float2 a = sm2[jj];
+        sx = a.x; sy = a.y;
+    } else {
+        const float4 a = sm_a[jj];
+        sx = a.x; sy = a.y; sz = a.z;
+    }
+    (void)nu;
+    (void)lx; (void)ly; (void)lz;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+        f2x dx = sub_bc(X[gg], sx);
+        f2x dy = sub_bc(Y[gg], sy);
+        if constexpr (COARSE && LO) {
+            dx = sub_bc(dx, lx);
+            dy = sub_bc(dy, ly);
+        }
+        f2x r2 = fma2(dx, dx, eps2);
+        r2 = fma2(dy, dy, r2);
+        f2x dz = 0ull;
+        if constexpr (DIM == 3) {
+            dz = sub_bc(Z[gg], sz);
+            if constexpr (COARSE && LO) dz = sub_bc(dz, lz);
+            r2 = fma2(dz, dz, r2);
+        }
+        // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
+        f2x inv;
+        if constexpr (QPOW && POLY) {
+            float r0, r1;
+            upk(r2, r0, r1);
+            inv = ex2_poly2(mul_bc(pk(lg2_approx(r0), lg2_approx(r1)), cexp));
+            if constexpr (PAIR_NU) inv = mul_bc(inv, nu);
+        } else if constexpr (PAIR_NU) {
+            // all k representatives, the own one H(i) included: kernel (a)
+            // subtracts that term (Q25); nu folded into the
+            // batched reciprocal: nu/a = b * (nu * rcp(ab))
+            if ((BMASK >> gg) & 1) {
+                float r0, r1;
+                upk(r2, r0, r1);
+                const float ip = nu * rcp_approx(r0 * r1);
+                inv = mul_bc(pk(r1, r0), ip);
+            } else {
+                inv = mul_bc(inv_pair<QPOW, false>(r2, cexp), nu);
+            }
+        } else {
+            inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
+        }
+        TX[gg] = fma2(dx, inv, TX[gg]);
+        TY[gg] = fma2(dy, inv, TY[gg]);
+        if constexpr (DIM == 3) TZ[gg] = fma2(dz, inv, TZ[gg]);
+    }
+}
+
+// One shared-memory source tile (cnt sources) against the thread's targets.
 template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, int UNR, bool PAIR_NU, bool LO>
 __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const float4* sm_b, const f2x (&X)[G],
                                            const f2x (&Y)[G], const f2x (&Z)[G], f2x (&TX)[G], f2x (&TY)[G],
                                            f2x (&TZ)[G], float cexp) {
-    const f2x eps2 = pk(kEps2, kEps2);
-    const float2* sm2 = reinterpret_cast<const float2*>(sm_a);
-#pragma unroll UNR
-    for (int jj = 0; jj < cnt; ++jj) {
-        float sx, sy, sz = 0.f, lx = 0.f, ly = 0.f, lz = 0.f, nu = 1.f;
-        if constexpr (COARSE) {
-            const float4 a = sm_a[jj];
-            sx = a.x; sy = a.y; sz = a.z; nu = a.w;
-            if constexpr (LO) {
-                const float4 b = sm_b[jj];
-                lx = b.x; ly = b.y; lz = b.z;
-            }
-        } else if constexpr (DIM == 2) {
-            const float2 a = sm2[jj];
-            sx = a.x; sy = a.y;
-        } else {
-            const float4 a = sm_a[jj];
-            sx = a.x; sy = a.y; sz = a.z;
+    constexpr int PM = (QPOW && COARSE) ? (DIM == 3 ? MM_POLY_MASK3 : MM_POLY_MASK2) : 0;
+    int jj = 0;
+    if constexpr (PM != 0) {
+        // blocks of 8 sources with a fixed MUFU / polynomial split (Q29)
+#define MM_SRC(u) \
+    source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, ((PM >> (u)) & 1) != 0>(jj + (u), sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp)
+        for (; jj + 8 <= cnt; jj += 8) {
+            MM_SRC(0); MM_SRC(1); MM_SRC(2); MM_SRC(3); MM_SRC(4); MM_SRC(5); MM_SRC(6); MM_SRC(7);
         }
-        (void)nu;
-        (void)lx; (void)ly; (void)lz;
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-            f2x dx = sub_bc(X[gg], sx);
-            f2x dy = sub_bc(Y[gg], sy);
-            if constexpr (COARSE && LO) {
-                dx = sub_bc(dx, lx);
-                dy = sub_bc(dy, ly);
-            }
-            f2x r2 = fma2(dx, dx, eps2);
-            r2 = fma2(dy, dy, r2);
-            f2x dz = 0ull;
-            if constexpr (DIM == 3) {
-                dz = sub_bc(Z[gg], sz);
-                if constexpr (COARSE && LO) dz = sub_bc(dz, lz);
-                r2 = fma2(dz, dz, r2);
-            }
-            // groups whose bit is set in BMASK use the batched reciprocal (q = 0)
-            f2x inv;
-            if constexpr (PAIR_NU) {
-                // all k representatives, the own one H(i) included: kernel (a)
-                // subtracts that term (Q25); nu folded into the
-                // batched reciprocal: nu/a = b * (nu * rcp(ab))
-                if ((BMASK >> gg) & 1) {
-                    float r0, r1;
-                    upk(r2, r0, r1);
-                    const float ip = nu * rcp_approx(r0 * r1);
-                    inv = mul_bc(pk(r1, r0), ip);
-                } else {
-                    inv = mul_bc(inv_pair<QPOW, false>(r2, cexp), nu);
-                }
-            } else {
-                inv = ((BMASK >> gg) & 1) ? inv_pair<QPOW, true>(r2, cexp) : inv_pair<QPOW, false>(r2, cexp);
-            }
-            TX[gg] = fma2(dx, inv, TX[gg]);
-            TY[gg] = fma2(dy, inv, TY[gg]);
-            if constexpr (DIM == 3) TZ[gg] = fma2(dz, inv, TZ[gg]);
-        }
+#undef MM_SRC
     }
+#pragma unroll UNR
+    for (; jj < cnt; ++jj)
+        source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, false>(jj, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp);
 }
 
 template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4>
@@ -166,6 +226,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
         f2x X[G], Y[G], Z[G], AX[G], AY[G], AZ[G];
         const int64_t base = (int64_t)tb * TPB;
         float wlo[3] = {INFINITY, INFINITY, INFINITY}, whi[3] = {-INFINITY, -INFINITY, -INFINITY};
+        const float4 fr = (COARSE && co.frame != nullptr) ? __ldg(co.frame) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
             const int64_t ia = tslot(base, gg, 0), ib = tslot(base, gg, 1);
@@ -179,8 +240,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             // the halves and force MOVs to re-form the pair at every use)
             const float* pa = x + ca * stride;
             const float* pb = x + cb * stride;
-            const float xa = __ldg(pa), xb = __ldg(pb), ya = __ldg(pa + 1), yb = __ldg(pb + 1);
-            const float za = DIM == 3 ? __ldg(pa + 2) : 0.f, zb = DIM == 3 ? __ldg(pb + 2) : 0.f;
+            // frame-relative targets: x - c is exact (c chosen by Sterbenz's rule, Q28)
+            const float xa = __ldg(pa) - fr.x, xb = __ldg(pb) - fr.x, ya = __ldg(pa + 1) - fr.y,
+                        yb = __ldg(pb + 1) - fr.y;
+            const float za = DIM == 3 ? __ldg(pa + 2) - fr.z : 0.f, zb = DIM == 3 ? __ldg(pb + 2) - fr.z : 0.f;
             X[gg] = pk(xa, xb);
             Y[gg] = pk(ya, yb);
             Z[gg] = (DIM == 3) ? pk(za, zb) : 0ull;
@@ -708,11 +771,17 @@ template <int DIM, bool QPOW, bool COARSE>
 #endif
 constexpr int kBatchMask = (DIM == 2 && !QPOW) ? (COARSE ? MM_COARSE_BMASK : 1) : 0;  // measured: tools/ubench_repulse.cu
 
+#ifndef MM_C3_MINB
+#define MM_C3_MINB 2  // 3-D q > 0 coarse kernel: at least 2 CTAs of 256 per SM (<= 128 registers)
+#endif
+template <int DIM, bool QPOW, bool COARSE>
+constexpr int kMinB = (DIM == 3 && QPOW && COARSE) ? MM_C3_MINB : 1;
+
 template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
     static const int occ = [] {  // per instantiation; queried once
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>, 1, MM_REP_UNR>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>, kMinB<DIM, QPOW, COARSE>, MM_REP_UNR>,
                                                       kBlock, 0);
         return o > 0 ? o : 1;
     }();
@@ -773,7 +842,7 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
 // batched reciprocals (BMASK) in half of the target groups for 2-D q = 0
 // (exact and coarse: measured faster by tools/ubench_repulse.cu); none for q > 0.
 #define MM_LAUNCH(D, Q, C, T) \
-    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>, 1, MM_REP_UNR><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, co, cexp,  \
+    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>, kMinB<D, Q, C>, MM_REP_UNR><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, co, cexp,  \
                                                                           p.sch, part)
     if (dim == 2) {
         if (!qpow && !coarse) MM_LAUNCH(2, false, false, MM_T2);

@@ -32,8 +32,8 @@ for name in sys.argv[1:] or ["cfg4"]:
     torch.cuda.synchronize()
     X = mm.coords_from_device(x, w.dim).astype(np.float64)
     H = mm.build_hierarchy(g, w.dim, w.seed)
-    p0 = H.copy_level(0)["parent"]
-    p1 = H.copy_level(1)["parent"]
+    p0 = H.level_host(0)["parent"]
+    p1 = H.level_host(1)["parent"]
     anc = p1[p0]
     k = int(anc.max()) + 1
     n, dim = X.shape
