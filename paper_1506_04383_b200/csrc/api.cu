@@ -379,7 +379,8 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     SymPlan sp;
     if (ap) {
         // frame origin of this sweep's positions (Q28); with per-sweep orders it comes with them
-        e = sb.reorder ? coarse_orders(n, dim, ap, x_in, sb, st) : launch_frame(dim, n, x_in, sb.box, sb.frame, st);
+        e = sb.reorder ? coarse_orders(n, dim, ap, x_in, sb, st)
+                       : launch_frame_fused(dim, n, x_in, sb.box, sb.frame, st);
         if (e != cudaSuccess) return e;
         e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, sb.frame, sb.rep_hi, sb.rep_lo,
                             far_tiles() ? sb.tile_box : nullptr, kCoarseTile, st);

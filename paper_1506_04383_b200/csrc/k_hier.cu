@@ -365,7 +365,7 @@ __device__ __forceinline__ float ord2f(uint32_t u) {
 }
 __global__ void k_box_init(uint32_t* box) {
     if (threadIdx.x < 3) box[threadIdx.x] = 0xffffffffu;
-    else if (threadIdx.x < 6) box[threadIdx.x] = 0u;
+    else if (threadIdx.x < 8) box[threadIdx.x] = 0u;  // [6]: ticket of k_frame_fused
 }
 template <int DIM>
 __global__ void k_bbox(int32_t n, const float* __restrict__ x, uint32_t* __restrict__ box) {
@@ -447,6 +447,58 @@ __global__ void k_target_keys(int32_t n, const float* __restrict__ x, const uint
                               uint32_t* __restrict__ key) {
     const int32_t i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) key[i] = morton_key<DIM>(load_x<DIM>(x, i), box);
+}
+// bounding box + frame origin in one launch: per-block min/max -> atomics on box;
+// the last block (ticket box[6]) derives the frame and re-arms box / ticket for
+// the next launch (box must be armed once by k_box_init)
+template <int DIM>
+__global__ void k_frame_fused(int32_t n, const float* __restrict__ x, uint32_t* __restrict__ box,
+                              float4* __restrict__ frame) {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const float4 p = load_x<DIM>(x, i);
+        const float v[3] = {p.x, p.y, p.z};
+#pragma unroll
+        for (int c = 0; c < DIM; ++c) {
+            mn[c] = fminf(mn[c], v[c]);
+            mx[c] = fmaxf(mx[c], v[c]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mn[c] = fminf(mn[c], __shfl_xor_sync(0xffffffffu, mn[c], o));
+            mx[c] = fmaxf(mx[c], __shfl_xor_sync(0xffffffffu, mx[c], o));
+        }
+        if ((threadIdx.x & 31) == 0 && mn[c] <= mx[c]) {
+            atomicMin(box + c, f2ord(mn[c]));
+            atomicMax(box + 3 + c, f2ord(mx[c]));
+        }
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ bool last;
+    if (threadIdx.x == 0) last = atomicAdd(box + 6, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last || threadIdx.x != 0) return;
+    __threadfence();
+    uint32_t b[6];
+    for (int c = 0; c < 6; ++c) b[c] = atomicAdd(box + c, 0u);  // coherent reads
+    float cc[3] = {0.f, 0.f, 0.f};
+    for (int a = 0; a < DIM; ++a) {
+        const float lo = ord2f(b[a]), hi = ord2f(b[3 + a]);
+        if (!(lo <= hi)) continue;
+        const float m = 0.5f * lo + 0.5f * hi;
+        const bool ok = (lo > 0.f && 0.5f * m <= lo && hi <= 2.0f * m) || (hi < 0.f && 0.5f * m >= hi && lo >= 2.0f * m);
+        cc[a] = ok ? m : 0.f;
+    }
+    *frame = make_float4(cc[0], cc[1], cc[2], 0.f);
+    for (int c = 0; c < 3; ++c) {
+        box[c] = 0xffffffffu;
+        box[3 + c] = 0u;
+    }
+    box[6] = 0u;
 }
 // representative keys from its (frame-relative) centroid
 template <int DIM>
@@ -811,6 +863,14 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
     return cudaGetLastError();
 }
 
+cudaError_t launch_frame_fused(int dim, int32_t n, const float* x, uint32_t* box, float4* frame, cudaStream_t st) {
+    LaunchScope ls("frame", st);
+    const int nb = std::max(1, std::min(nblk(n), 2 * 148));
+    if (dim == 2) k_frame_fused<2><<<nb, 256, 0, st>>>(n, x, box, frame);
+    else k_frame_fused<3><<<nb, 256, 0, st>>>(n, x, box, frame);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_frame(int dim, int32_t n, const float* x, uint32_t* box, float4* frame, cudaStream_t st) {
     LaunchScope ls("frame", st);
     k_box_init<<<1, 32, 0, st>>>(box);
@@ -857,6 +917,7 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
     LaunchScope ls("order_slots", st);
     k_scatter_inv<<<nblk(n), 256, 0, st>>>(n, tperm, tpos);
     k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, rkey_sorted, rpos, tile_nu, tile);
+    k_box_init<<<1, 32, 0, st>>>(box);  // armed for launch_frame_fused
     return cudaGetLastError();
 }
 

@@ -36,6 +36,8 @@ cudaError_t launch_compose(int32_t n, const int32_t* a, const int32_t* map, int3
 // Frame origin of kernel (c) (Q28): box = bounding box of x (uint32[6]
 // order-preserving scratch); frame->xyz = per-axis origin c with x - c exact in FP32, or 0
 cudaError_t launch_frame(int dim, int32_t n, const float* x, uint32_t* box, float4* frame, cudaStream_t st);
+// the same in one launch; box must hold the armed state left by launch_frame / a previous fused launch
+cudaError_t launch_frame_fused(int dim, int32_t n, const float* x, uint32_t* box, float4* frame, cudaStream_t st);
 // Orders for kernel (c) (Q26, Q27) from the positions x (also computes the frame):
 //  targets: tperm[slot] = vertex id in Morton order of x (tpos = inverse);
 //  representatives: rord[slot] = rep id ordered by (mass nu, Morton key of its centroid),

@@ -386,6 +386,10 @@ constexpr int sym_smem_bytes(int warps) {
 #define MM_SYM_UNR 8
 #endif
 constexpr int kSymUnroll = MM_SYM_UNR;
+#ifndef MM_SYM_JPACK
+#define MM_SYM_JPACK 0  // 1: j-side sums as packed per-step partials (FFMA2); measured 2% slower at cfg2
+#endif
+constexpr bool kSymJPack = MM_SYM_JPACK != 0;
 // one 32-step rotation over a chunk of 32 sources; MASK: the chunk is the
 // partial tail of the last block (lanes past the end carry weight 0)
 template <int DIM, bool QPOW, int SG, bool MASK>
@@ -398,6 +402,8 @@ __device__ __forceinline__ void sym_chunk(const f2x (&X)[SG], const f2x (&Y)[SG]
     const int nxt = (lane + 1) & 31;
 #pragma unroll kSymUnroll
     for (int k = 0; k < 32; ++k) {
+        f2x PX = 0ull, PY = 0ull, PZ = 0ull;
+        (void)PX; (void)PY; (void)PZ;
 #pragma unroll
         for (int gg = 0; gg < SG; ++gg) {
             const f2x dx = sub_bc(X[gg], sx), dy = sub_bc(Y[gg], sy);
@@ -414,18 +420,43 @@ __device__ __forceinline__ void sym_chunk(const f2x (&X)[SG], const f2x (&Y)[SG]
             AY[gg] = fma2(dy, inv, AY[gg]);
             if constexpr (DIM == 3) AZ[gg] = fma2(dz, inv, AZ[gg]);
             // j side: sum_t (x_j - x_t) inv_t = -sum_t dx_t inv_t
-            float i0, i1, a0, a1;
-            upk(inv, i0, i1);
-            upk(dx, a0, a1);
-            bx = fmaf(-a0, i0, bx);
-            bx = fmaf(-a1, i1, bx);
-            upk(dy, a0, a1);
-            by = fmaf(-a0, i0, by);
-            by = fmaf(-a1, i1, by);
+            if constexpr (kSymJPack) {
+                // packed per-step partials (one FFMA2 per component and packed pair),
+                // folded into the rotating scalar sums after the step
+                if (gg == 0) {
+                    PX = mul2(dx, inv);
+                    PY = mul2(dy, inv);
+                    if constexpr (DIM == 3) PZ = mul2(dz, inv);
+                } else {
+                    PX = fma2(dx, inv, PX);
+                    PY = fma2(dy, inv, PY);
+                    if constexpr (DIM == 3) PZ = fma2(dz, inv, PZ);
+                }
+            } else {
+                float i0, i1, a0, a1;
+                upk(inv, i0, i1);
+                upk(dx, a0, a1);
+                bx = fmaf(-a0, i0, bx);
+                bx = fmaf(-a1, i1, bx);
+                upk(dy, a0, a1);
+                by = fmaf(-a0, i0, by);
+                by = fmaf(-a1, i1, by);
+                if constexpr (DIM == 3) {
+                    upk(dz, a0, a1);
+                    bz = fmaf(-a0, i0, bz);
+                    bz = fmaf(-a1, i1, bz);
+                }
+            }
+        }
+        if constexpr (kSymJPack) {
+            float p0, p1;
+            upk(PX, p0, p1);
+            bx -= p0 + p1;
+            upk(PY, p0, p1);
+            by -= p0 + p1;
             if constexpr (DIM == 3) {
-                upk(dz, a0, a1);
-                bz = fmaf(-a0, i0, bz);
-                bz = fmaf(-a1, i1, bz);
+                upk(PZ, p0, p1);
+                bz -= p0 + p1;
             }
         }
         // rotate the source and its accumulator: lane l takes lane l+1's
