@@ -418,7 +418,9 @@ def run_gpu(args):
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tj = json.load(f)
-        if kname in tj and w.name in tj[kname].get("workload", ""):
+        if kname in tj and w.name in tj[kname].get("by_config", {}):
+            traffic = tj[kname]["by_config"][w.name]
+        elif kname in tj and w.name in tj[kname].get("workload", ""):
             traffic = tj[kname]["bytes"]
     except (OSError, ValueError, KeyError):
         traffic = None
