@@ -231,6 +231,7 @@ struct SweepBufs {
     uint32_t* box = nullptr;     // [8] layout box (scratch)
     float4* frame = nullptr;     // [1] kernel (c)'s frame origin (Q28)
     bool reorder = false;        // recompute kernel (c)'s orders before every sweep
+    bool far = false;            // kernel (c) with per-sweep frame and tile boxes (lo-free far tiles, Q27/Q28)
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
 };
@@ -356,6 +357,17 @@ bool reorder_every_sweep(int32_t n, int32_t k) {
     return (double)n * (double)k >= thr;
 }
 
+// The far-tile machinery costs two small launches per sweep (frame, tile boxes):
+// below this many pairs per sweep (kernel (c) well under ~0.3 ms) it does not pay
+// (MM_FAR_PAIRS overrides; measured in the MulMent_7/10 schedules, small k)
+double far_min_pairs() {
+    static const double thr = [] {
+        const char* v = getenv("MM_FAR_PAIRS");
+        return v ? atof(v) : 1e9;
+    }();
+    return thr;
+}
+
 // Group maps into CSRs (members of each representative, children of each parent).
 cudaError_t prepare_approx(int32_t n, int dim, const mm_approx* ap, const float* x, SweepBufs& sb, cudaStream_t st) {
     cudaError_t e = group_by_key(n, ap->ancestor, ap->k, sb.mptr, sb.mem, sb.key_sorted, sb.iota, sb.cnt, sb.tmp,
@@ -364,6 +376,7 @@ cudaError_t prepare_approx(int32_t n, int dim, const mm_approx* ap, const float*
     e = group_by_key(n, ap->parent, n, sb.cptr, sb.child, sb.key_sorted, sb.iota, sb.cnt, sb.tmp, sb.tmp_bytes, st);
     if (e != cudaSuccess) return e;
     sb.reorder = reorder_every_sweep(n, ap->k);
+    sb.far = far_tiles() && (double)n * (double)ap->k >= far_min_pairs();
     return coarse_orders(n, dim, ap, x, sb, st);
 }
 
@@ -379,18 +392,19 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     SymPlan sp;
     if (ap) {
         // frame origin of this sweep's positions (Q28); with per-sweep orders it comes with them
-        e = sb.reorder ? coarse_orders(n, dim, ap, x_in, sb, st)
-                       : launch_frame_fused(dim, n, x_in, sb.box, sb.frame, st);
+        if (sb.reorder) e = coarse_orders(n, dim, ap, x_in, sb, st);
+        else if (sb.far) e = launch_frame_fused(dim, n, x_in, sb.box, sb.frame, st);
         if (e != cudaSuccess) return e;
-        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, sb.frame, sb.rep_hi, sb.rep_lo,
-                            far_tiles() ? sb.tile_box : nullptr, kCoarseTile, st);
+        const float4* frame = sb.far ? sb.frame : nullptr;
+        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, frame, sb.rep_hi, sb.rep_lo,
+                            sb.far ? sb.tile_box : nullptr, kCoarseTile, st);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
         CoarseOrder co;
         co.tperm = sb.tperm;
         co.tile_nu = sb.tile_nu;
-        co.tile_box = far_tiles() ? sb.tile_box : nullptr;
-        co.frame = sb.frame;
+        co.tile_box = sb.far ? sb.tile_box : nullptr;
+        co.frame = frame;
         e = launch_repulse(dim, qpow, true, q, n, x_in, ap->k, sb.rep_hi, sb.rep_lo, co, p, sb.part, st);
     } else if (sb.jpart) {
         sp = plan_repulse_sym(n, dim);
@@ -423,7 +437,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         ga.anc = ap->ancestor;
         ga.rpos = sb.rpos;
         ga.tpos = sb.tpos;
-        ga.frame = sb.frame;
+        ga.frame = sb.far ? sb.frame : nullptr;
         ga.rep_hi = sb.rep_hi;
         ga.rep_lo = sb.rep_lo;
     }

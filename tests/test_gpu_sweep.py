@@ -320,9 +320,11 @@ def test_exact_sweep_3d_symmetric_sampled(mm, n, q):
 @pytest.mark.parametrize("offset", [0.0, 2.0e4])
 def test_approx_far_tiles_structured_layout(mm, offset):
     """Eq.(3) on a layout with spatially compact clusters (the mesh drawn on its
-    grid, jittered), so most (warp, tile) pairs take kernel (c)'s lo-free far
-    path (Q27); translated by `offset` the threshold 2^-7 X grows and
-    more tiles keep hi/lo.  All rows against the oracle."""
+    grid, jittered), so that with the far-tile path on (MM_FAR_PAIRS=1 in
+    test_gpu_coarse_modes.py; off at this size by default) most (warp, tile)
+    pairs take kernel (c)'s lo-free far path (Q27); translated by
+    `offset` the frame origin (Q28) moves to the layout.  All rows against the
+    oracle."""
     w = workload("cfg3_mesh128")
     lv = oracle_hierarchy("cfg3_mesh128")
     anc = oracle.ancestor(lv, 0, 2)
