@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 // repulsion partials of this vertex (static schedule slots), fetched
                 // first so that their latency overlaps the S-row loads
                 const int stride = DIM == 2 ? 2 : 4;
-                // kernel (c) writes partials by target slot (spatial order, Q27)
+                // kernel (c) processes targets by slot (spatial order, Q27): the slot
+                // count follows the slot's block; the partials sit at the vertex id
                 const int64_t pi = a.tpos != nullptr ? (int64_t)__ldg(a.tpos + i) : i;
                 const int64_t tb = pi / a.tpb;
                 const int32_t nslot =
@@ -89,7 +90,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                             : sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
                                   sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
                 for (int p = 0; p < nslot; ++p) {
-                    const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, pi);
+                    const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
                     R.x += v.x;
                     R.y += v.y;
                     R.z += v.z;

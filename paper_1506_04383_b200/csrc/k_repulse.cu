@@ -343,8 +343,12 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             upk(AX[gg], ax0, ax1);
             upk(AY[gg], ay0, ay1);
             if constexpr (DIM == 3) upk(AZ[gg], az0, az1);
-            if (ia < n_tgt) store_x<DIM>(out, ia, make_float4(ax0, ay0, az0, 0.f));
-            if (ib < n_tgt) store_x<DIM>(out, ib, make_float4(ax1, ay1, az1, 0.f));
+            // stored at the vertex id (spatial order: tperm), so that kernel (a) reads
+            // its slots coalesced
+            if (ia < n_tgt) store_x<DIM>(out, (COARSE && co.tperm) ? (int64_t)__ldg(co.tperm + ia) : ia,
+                                         make_float4(ax0, ay0, az0, 0.f));
+            if (ib < n_tgt) store_x<DIM>(out, (COARSE && co.tperm) ? (int64_t)__ldg(co.tperm + ib) : ib,
+                                         make_float4(ax1, ay1, az1, 0.f));
         }
         u = seg_end;
     }
@@ -651,6 +655,30 @@ __device__ __forceinline__ float entropy_phi2(float a, float b, float cq) {
     }
 }
 
+#ifndef MM_ENT_POLY
+#define MM_ENT_POLY 1  // q > 0 energy: the second target pair of every other source uses ex2_poly2 (Q29)
+#endif
+// one source against the thread's 2 x 2 targets (no mask); POLY1: 2^y of group 1 on the FMA pipe
+template <int DIM, bool QPOW, bool POLY1>
+__device__ __forceinline__ void entropy_src(const float4& sv, const f2x (&X)[2], const f2x (&Y)[2],
+                                            const f2x (&Z)[2], float cq, float& acc, int32_t& zt) {
+#pragma unroll
+    for (int gg = 0; gg < 2; ++gg) {
+        float ra, rb;
+        upk(entropy_r2<DIM>(X[gg], Y[gg], Z[gg], sv), ra, rb);
+        zt += (ra == 0.f) + (rb == 0.f);
+        ra = fmaxf(ra, kR2Floor);
+        rb = fmaxf(rb, kR2Floor);
+        if (QPOW && POLY1 && gg == 1) {
+            float ea, eb;
+            upk(ex2_poly2(mul_bc(pk(lg2_approx(ra), lg2_approx(rb)), cq)), ea, eb);
+            acc += ea + eb;
+        } else {
+            acc += entropy_phi2<QPOW>(ra, rb, cq);
+        }
+    }
+}
+
 template <int DIM, bool QPOW>
 __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* __restrict__ x, float cq,
                                                         TriSched ts, double* __restrict__ partial,
@@ -734,17 +762,16 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
                     }
                 }
             } else if (!diag) {
-#pragma unroll 4
-                for (int jj = 0; jj < cnt; ++jj) {
-                    const float4 sv = sm[jj];
-#pragma unroll
-                    for (int gg = 0; gg < G; ++gg) {
-                        float ra, rb;
-                        upk(entropy_r2<DIM>(X[gg], Y[gg], Z[gg], sv), ra, rb);
-                        zt += (ra == 0.f) + (rb == 0.f);
-                        acc += entropy_phi2<QPOW>(fmaxf(ra, kR2Floor), fmaxf(rb, kR2Floor), cq);
+                int jj = 0;
+                if constexpr (QPOW && MM_ENT_POLY) {
+#pragma unroll 2
+                    for (; jj + 2 <= cnt; jj += 2) {
+                        entropy_src<DIM, QPOW, false>(sm[jj], X, Y, Z, cq, acc, zt);
+                        entropy_src<DIM, QPOW, true>(sm[jj + 1], X, Y, Z, cq, acc, zt);
                     }
                 }
+#pragma unroll 4
+                for (; jj < cnt; ++jj) entropy_src<DIM, QPOW, false>(sm[jj], X, Y, Z, cq, acc, zt);
             } else {
                 for (int jj = 0; jj < cnt; ++jj) {
                     const float4 sv = sm[jj];

@@ -54,7 +54,7 @@ struct EntropyPlan {
 
 // Orders / metadata of kernel (c) (all nullable; Q26, Q27)
 struct CoarseOrder {
-    const int32_t* tperm = nullptr;    // target slot -> vertex id (spatial order); partials are written by slot
+    const int32_t* tperm = nullptr;    // target slot -> vertex id (spatial order); partials are written at the vertex id
     const int32_t* tile_nu = nullptr;  // [ceil(k/256)] common mass nu of a source tile, or 0 (mixed)
     const float4* tile_box = nullptr;  // [2 ceil(k/256)] box of a tile's hi coordinates (.w of [0]: max |coord|)
     const float4* frame = nullptr;     // origin c: targets are x - c (exact, Q28); representatives are frame-relative
@@ -92,7 +92,7 @@ struct GatherArgs {
     // all k representatives (nullable: exact mode)
     const int32_t* anc = nullptr;
     const int32_t* rpos = nullptr;  // nullable: slot of representative v in rep_hi/rep_lo (mass order)
-    const int32_t* tpos = nullptr;  // nullable: slot of vertex i in kernel (c)'s partials (spatial order)
+    const int32_t* tpos = nullptr;  // nullable: slot of vertex i in kernel (c)'s schedule (spatial order)
     const float4* frame = nullptr;  // nullable: origin of the frame-relative representatives (Q28)
     const float4* rep_hi = nullptr;
     const float4* rep_lo = nullptr;
