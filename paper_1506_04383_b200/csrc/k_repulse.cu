@@ -832,8 +832,11 @@ constexpr int kBatchMask = (DIM == 2 && !QPOW) ? (COARSE ? MM_COARSE_BMASK : 1) 
 #ifndef MM_C3_MINB
 #define MM_C3_MINB 2  // 3-D q > 0 coarse kernel: at least 2 CTAs of 256 per SM (<= 128 registers)
 #endif
+#ifndef MM_C2_MINB
+#define MM_C2_MINB 1  // 2-D coarse kernel: CTAs of 256 per SM the register budget must allow
+#endif
 template <int DIM, bool QPOW, bool COARSE>
-constexpr int kMinB = (DIM == 3 && QPOW && COARSE) ? MM_C3_MINB : 1;
+constexpr int kMinB = (DIM == 3 && QPOW && COARSE) ? MM_C3_MINB : (DIM == 2 && COARSE) ? MM_C2_MINB : 1;
 
 template <int DIM, bool QPOW, bool COARSE, int T>
 int resident_ctas() {
