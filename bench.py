@@ -473,7 +473,10 @@ def run_gpu(args):
                                         "grid barriers per sweep)") if small else ("symmetric" if sym else "one-sided"),
                      "executed_flop_per_pair": exec_flop_pair,
                      "executed_tflops": executed_tflops, "executed_frac": executed_tflops / FP32_PEAK_TFLOPS,
-                     "mufu_ceiling_frac": None if sym else MUFU_PER_CLK_SM * FLOP_PER_PAIR / (2.0 * FP32_LANES),
+                     # the frac a kernel reaches at 16 MUFU ops/clk/SM with one MUFU per pair (q = 0)
+                     # or two (q > 0: lg2 + ex2), before batching / polynomial 2^y (Q29)
+                     "mufu_ceiling_frac": None if sym else
+                     MUFU_PER_CLK_SM / (2.0 if w.q != 0.0 else 1.0) * flop_pair / (2.0 * FP32_LANES),
                      "pairs_per_s_kernel": pairs_launch / (k_ms / 1e3)},
         "levels": rep["n_level"], "k_levels": rep["k_level"],
         "kernel_share_of_step": step_share,

@@ -1,7 +1,7 @@
 """Fraction of (warp, source tile) pairs of kernel (c) that take the lo-free far
 path (Q27) on the final finest-level layout of a config, for several
-thresholds 2^-b X.  Orders and boxes are recomputed here on the host (numpy)
-the way approx_orders / k_tile_box define them.
+thresholds 2^-b X.  Orders, frame origin (Q28) and boxes are recomputed here on
+the host (numpy) the way approx_orders / k_frame / k_tile_box define them.
 Usage: python tools/far_fraction.py cfg4 [cfg3 ...]"""
 import os
 import sys
@@ -39,12 +39,15 @@ for name in sys.argv[1:] or ["cfg4"]:
     n, dim = X.shape
     nu = np.bincount(anc, minlength=k)
     cen = np.stack([np.bincount(anc, weights=X[:, c], minlength=k) for c in range(dim)], 1) / nu[:, None]
-    first = np.full(k, n, np.int64)
-    np.minimum.at(first, anc, np.arange(n))
     lo, hi = X.min(0), X.max(0)
     bits = 16 if dim == 2 else 10
     tord = np.argsort(morton(X, lo, hi, bits), kind="stable")
-    rkey = (nu.astype(np.int64) << 32) | morton(X[first], lo, hi, bits)
+    rkey = (nu.astype(np.int64) << 32) | morton(cen, lo, hi, bits)
+    # frame origin (Q28): box midpoint where it keeps x - c exact, else 0
+    m = 0.5 * lo + 0.5 * hi
+    c = np.where(((lo > 0) & (0.5 * m <= lo) & (hi <= 2 * m)) | ((hi < 0) & (0.5 * m >= hi) & (lo >= 2 * m)), m, 0.0)
+    X = X - c
+    cen = cen - c
     rord = np.argsort(rkey, kind="stable")
     T = 128 if dim == 2 else 64
     nw = (n + T - 1) // T

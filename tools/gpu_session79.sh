@@ -1,0 +1,10 @@
+# final round-1 refresh: full GPU suite, headline bench, launch list, far fractions after Q28
+mkdir -p gpurun_out/s79
+timeout 1800 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/s79/pytest.log 2>&1; tail -3 gpurun_out/s79/pytest.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 600 python bench.py > gpurun_out/s79/bench_cfg2.json 2> gpurun_out/s79/e2.err; echo bench rc=$?
+python -c "
+import json; d=json.load(open('gpurun_out/s79/bench_cfg2.json')); r=d['roofline']
+print('cfg2 ms %.2f'%d['ms_per_step'], 'value %.4g'%d['value'], 'frac %.3f'%r['frac'], 'e2e %.4g'%d['e2e']['value'], d['clocks'])"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s79/r01_launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/s79/ncul2.log 2>&1; echo ncul2=$?
+timeout 1200 python tools/far_fraction.py cfg3 cfg4 cfg5 2>&1 | grep -v Warn
