@@ -8,3 +8,12 @@ import json; d=json.load(open('gpurun_out/s79/bench_cfg2.json')); r=d['roofline'
 print('cfg2 ms %.2f'%d['ms_per_step'], 'value %.4g'%d['value'], 'frac %.3f'%r['frac'], 'e2e %.4g'%d['e2e']['value'], d['clocks'])"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/s79/r01_launches_cfg2.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/s79/ncul2.log 2>&1; echo ncul2=$?
 timeout 1200 python tools/far_fraction.py cfg3 cfg4 cfg5 2>&1 | grep -v Warn
+mkdir -p gpurun_out/s79/r01_bench
+cp gpurun_out/s79/bench_cfg2.json gpurun_out/s79/r01_bench/
+timeout 900 python bench.py --config cfg3 --steps 3 --warmup 3 > gpurun_out/s79/r01_bench/bench_cfg3.json 2>/dev/null; echo cfg3 rc=$?
+timeout 1200 python bench.py --config cfg4 --steps 2 --warmup 3 > gpurun_out/s79/r01_bench/bench_cfg4.json 2>/dev/null; echo cfg4 rc=$?
+timeout 1500 python bench.py --config cfg5 --steps 2 --warmup 3 > gpurun_out/s79/r01_bench/bench_cfg5.json 2>/dev/null; echo cfg5 rc=$?
+timeout 600 python bench.py --config cfg1 > gpurun_out/s79/r01_bench/bench_cfg1.json 2>/dev/null; echo cfg1 rc=$?
+for c in 1 2 3 4 5; do python -c "
+import json; d=json.load(open('gpurun_out/s79/r01_bench/bench_cfg$c.json')); r=d['roofline']
+print('cfg$c ms %.2f'%d['ms_per_step'], 'value %.4g'%d['value'], r.get('kernel'), 'frac %.3f'%r['frac'], 'mufu_ceil', r.get('mufu_ceiling_frac'), 'pairs/s %.4g'%r.get('pairs_per_s_kernel', 0), 'e2e %.4g'%d['e2e'].get('value'), d['clocks'])"; done
