@@ -197,15 +197,20 @@ def sweep_approx(S, x: np.ndarray, alpha: float, q: float, parent: np.ndarray, a
     return out
 
 
-def energy(S, x: np.ndarray, alpha: float, q: float, nthreads: Optional[int] = None):
-    """Eq.(1) (P:163-171, Q3/Q4): returns (stress, entropy, total)."""
+def energy(S, x: np.ndarray, alpha: float, q: float, nthreads: Optional[int] = None,
+           skip_coincident: bool = False):
+    """Eq.(1) (P:163-171, Q3/Q4): returns (stress, entropy, total).
+    A coincident non-S pair is an error, unless skip_coincident: then
+    such pairs are left out of the entropy, as mm_layout's report does (Q6)."""
     rp, col, d, w = _csr(S)
     x = np.ascontiguousarray(x, dtype=np.float64)
     n, dim = x.shape
     out = np.zeros(3, dtype=np.float64)
-    _check(lib().or_energy(n, dim, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
-                           _p(d, ctypes.c_double), _p(w, ctypes.c_double), _p(x, ctypes.c_double),
-                           alpha, q, _p(out, ctypes.c_double), nthreads or default_threads()), "energy")
+    rc = lib().or_energy(n, dim, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+                         _p(d, ctypes.c_double), _p(w, ctypes.c_double), _p(x, ctypes.c_double),
+                         alpha, q, _p(out, ctypes.c_double), nthreads or default_threads())
+    if not (skip_coincident and rc == -3):
+        _check(rc, "energy")
     return float(out[0]), float(out[1]), float(out[2])
 
 

@@ -31,10 +31,14 @@ for name in sys.argv[1:] or ["cfg2", "cfg3"]:
     xo, eo, nl = oracle.layout(w.graph, w.S, w.dim, w.alpha, w.q, w.h, [w.sweeps], w.seed,
                                x_init=None if w.h > 0 else w.x0.astype(np.float64))
     t_or = time.perf_counter() - t
-    eg = oracle.energy(w.S, xg.astype(np.float64), w.alpha, w.q)
     rel = abs(rep["energy"] - eo[2]) / abs(eo[2])
-    print(json.dumps({"config": name, "n": w.n, "levels_gpu": rep["levels"], "levels_oracle": nl,
-                      "E_gpu": rep["energy"], "E_oracle": eo[2], "rel_diff": rel, "within_1e-3": rel <= 1e-3,
-                      "E_oracle_of_gpu_layout": eg[2], "rel_kernel": abs(rep["energy"] - eg[2]) / abs(eg[2]),
-                      "stress_gpu": rep["stress"], "stress_oracle": eo[0],
-                      "gpu_s": t_gpu, "oracle_s": t_or, "oracle_threads": oracle.default_threads()}), flush=True)
+    res = {"config": name, "n": w.n, "levels_gpu": rep["levels"], "levels_oracle": nl,
+           "E_gpu": rep["energy"], "E_oracle": eo[2], "rel_diff": rel, "within_1e-3": rel <= 1e-3,
+           "stress_gpu": rep["stress"], "stress_oracle": eo[0], "coincident_pairs_gpu": rep["coincident_pairs"],
+           "gpu_s": t_gpu, "oracle_s": t_or, "oracle_threads": oracle.default_threads()}
+    print(json.dumps(res), flush=True)
+    # kernel error alone: the oracle's energy of the GPU layout; FP32 layouts can hold exactly
+    # coincident vertices (leaves of one hub), left out as the GPU report does (Q6)
+    eg = oracle.energy(w.S, xg.astype(np.float64), w.alpha, w.q, skip_coincident=True)
+    res.update({"E_oracle_of_gpu_layout": eg[2], "rel_kernel": abs(rep["energy"] - eg[2]) / abs(eg[2])})
+    print(json.dumps(res), flush=True)
