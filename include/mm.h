@@ -174,7 +174,14 @@ MM_API mm_status mm_sweep_workspace(int32_t n, int dim, const mm_approx* ap, siz
  * unweighted means of x_in over each H class (Q11/Q12).
  * x_out must not alias x_in.  ws/ws_bytes: caller scratch of at least
  * mm_sweep_workspace() bytes, or NULL/0 to let the library allocate it
- * stream-ordered.  stats (device, nullable) receives mm_sweep_stats.  async. */
+ * stream-ordered.  stats (device, nullable) receives mm_sweep_stats.  async.
+ * Eq.(3) evaluation order (results equal up to FP32 rounding, DESIGN.md
+ * Q26-Q28): targets and representatives are visited in spatial order and
+ * representatives grouped by mass; tiles far from a warp's targets drop the
+ * FP64 lo part of the centroids.  Environment (read once per process, tests
+ * and experiments): MM_FAR_TILES=0 keeps hi/lo everywhere, MM_FAR_PAIRS /
+ * MM_REORDER_PAIRS set the n k thresholds of the far-tile path (1e9) and of
+ * per-sweep re-sorting (1e11). */
 MM_API mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap,
                    const float* x_in, float* x_out, mm_sweep_stats* stats,
                    void* ws, size_t ws_bytes, mm_stream_t stream);
