@@ -479,6 +479,11 @@ def run_gpu(args):
                      MUFU_PER_CLK_SM / (2.0 if w.q != 0.0 else 1.0) * flop_pair / (2.0 * FP32_LANES),
                      "pairs_per_s_kernel": pairs_launch / (k_ms / 1e3)},
         "levels": rep["n_level"], "k_levels": rep["k_level"],
+        # what the timed step computed (last step's report): Eq.(1) of the final layout (coincident
+        # non-S pairs, possible in FP32, are left out and counted: DESIGN.md Q6) and the last sweep's
+        # relative change
+        "result": {"energy": rep["energy"], "stress": rep["stress"], "entropy": rep["entropy"],
+                   "coincident_pairs": rep["coincident_pairs"], "rel_change": rep["rel_change"]},
         "kernel_share_of_step": step_share,
         "kernel_share_of_gpu_time": gpu_share,
         "kernels": prof,
