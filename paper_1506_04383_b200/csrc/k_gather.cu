@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 // kernel (c) processes targets by slot (spatial order, Q27): the slot
                 // count follows the slot's block; the partials sit at the vertex id
                 const int64_t pi = a.tpos != nullptr ? (int64_t)__ldg(a.tpos + i) : i;
-                const int64_t tb = pi / a.tpb;
+                const int64_t tb = (int32_t)pi / a.tpb;  // pi < n < 2^31: 32-bit division
                 const int32_t nslot =
                     a.jpart ? sched_first_cta_tri(tri_prefix((int32_t)tb + 1, a.tri) - 1, a.tri) -
                                   sched_first_cta_tri(tri_prefix((int32_t)tb, a.tri), a.tri) + 1

@@ -15,9 +15,26 @@ struct Sched {
     int32_t TB = 1;   // target blocks
     int32_t G = 1;    // CTAs
 };
+#ifndef MM_FASTDIV
+#define MM_FASTDIV 1
+#endif
+// floor(a / b) for 0 <= a < 2^53, b > 0.  On the device the quotient comes from
+// an FP64 division (a and b exact in double; the rounded quotient is within
+// one of the true one) plus one integer correction step: exact, and far cheaper
+// than the 64-bit integer division routine (kernel (a) evaluates three per vertex).
+__host__ __device__ __forceinline__ int64_t floor_div_nonneg(int64_t a, int64_t b) {
+#if defined(__CUDA_ARCH__) && MM_FASTDIV
+    int64_t q = (int64_t)((double)a / (double)b);
+    if (q * b > a) --q;
+    else if ((q + 1) * b <= a) ++q;
+    return q;
+#else
+    return a / b;
+#endif
+}
 // first CTA whose range contains work unit a: max{g : floor(g U / G) <= a}
 __host__ __device__ __forceinline__ int32_t sched_first_cta(int64_t a, const Sched& s) {
-    return (int32_t)(((a + 1) * (int64_t)s.G - 1) / s.U);
+    return (int32_t)floor_div_nonneg((a + 1) * (int64_t)s.G - 1, s.U);
 }
 
 struct RepulsePlan {
@@ -36,7 +53,7 @@ __host__ __device__ __forceinline__ int64_t tri_prefix(int32_t tb, const TriSche
 }
 // first CTA whose range of a triangular schedule contains unit a (same rule as sched_first_cta)
 __host__ __device__ __forceinline__ int32_t sched_first_cta_tri(int64_t a, const TriSched& s) {
-    return (int32_t)(((a + 1) * (int64_t)s.G - 1) / s.U);
+    return (int32_t)floor_div_nonneg((a + 1) * (int64_t)s.G - 1, s.U);
 }
 struct SymPlan {
     TriSched ts;        // blocks of 1024 vertices; units = (block pair (I, J >= I), source sub-tile)
