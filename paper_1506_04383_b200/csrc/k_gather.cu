@@ -55,6 +55,9 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
 #ifndef MM_GATHER_MINB
 #define MM_GATHER_MINB 4
 #endif
+#ifndef MM_GATHER_PREFETCH
+#define MM_GATHER_PREFETCH 1  // first-level indices of the next vertex loaded one iteration ahead
+#endif
 #ifndef MM_GATHER_UNROLL
 #define MM_GATHER_UNROLL 4
 #endif
@@ -65,11 +68,31 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
     const int lg = threadIdx.x & (G - 1);
     constexpr int VPB = kGBlock / G;  // vertices per block iteration
     double v_dx2 = 0.0, v_x2 = 0.0, v_st = 0.0;
+    // software pipeline over the grid-stride loop: the row bounds and the
+    // map entries of the NEXT vertex are loaded while this one is processed,
+    // which takes one level off each dependent chain (rp -> col -> x[col],
+    // parent -> child_ptr -> child -> x, anc -> rpos -> rep, tpos -> partials)
+    int64_t nx_e0 = 0, nx_e1 = 0;
+    int32_t nx_tp = 0, nx_par = 0, nx_anc = 0;
+    auto prefetch = [&](int64_t vb2) {
+        const int64_t i2 = vb2 + threadIdx.x / G;
+        if (MM_GATHER_PREFETCH && i2 < a.n) {
+            nx_e0 = a.rp[i2];
+            nx_e1 = a.rp[i2 + 1];
+            if (a.tpos != nullptr) nx_tp = __ldg(a.tpos + i2);
+            if (a.parent != nullptr) nx_par = __ldg(a.parent + i2);
+            if (a.anc != nullptr) nx_anc = __ldg(a.anc + i2);
+        }
+    };
+    prefetch((int64_t)blockIdx.x * VPB);
     // grid-stride over vertex chunks: a fixed number of CTAs -> a fixed,
     // small number of FP64 partials, each accumulated in a fixed order
     for (int64_t vb = (int64_t)blockIdx.x * VPB; vb < a.n; vb += (int64_t)gridDim.x * VPB) {
         const int64_t i = vb + threadIdx.x / G;
         const bool valid = i < a.n;
+        const int64_t cur_e0 = nx_e0, cur_e1 = nx_e1;
+        const int32_t cur_tp = nx_tp, cur_par = nx_par, cur_anc = nx_anc;
+        prefetch(vb + (int64_t)gridDim.x * VPB);
         float4 xi = make_float4(0.f, 0.f, 0.f, 0.f);
         float rho = 0.f, st = 0.f;
         float4 A = make_float4(0.f, 0.f, 0.f, 0.f), C = A;
@@ -82,7 +105,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 const int stride = DIM == 2 ? 2 : 4;
                 // kernel (c) processes targets by slot (spatial order, Q27): the slot
                 // count follows the slot's block; the partials sit at the vertex id
-                const int64_t pi = a.tpos != nullptr ? (int64_t)__ldg(a.tpos + i) : i;
+                const int64_t pi = a.tpos != nullptr ? (int64_t)(MM_GATHER_PREFETCH ? cur_tp : __ldg(a.tpos + i)) : i;
                 const int64_t tb = (int32_t)pi / a.tpb;  // pi < n < 2^31: 32-bit division
                 const int32_t nslot =
                     a.jpart ? sched_first_cta_tri(tri_prefix((int32_t)tb + 1, a.tri) - 1, a.tri) -
@@ -107,8 +130,8 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
             }
             // row i: 64-bit base, 32-bit offsets; the S arrays are read once per
             // sweep (streaming loads, evict-first) so that x stays in L2
-            const int64_t e0 = a.rp[i];
-            const int len = (int)(a.rp[i + 1] - e0);
+            const int64_t e0 = MM_GATHER_PREFETCH ? cur_e0 : a.rp[i];
+            const int len = (int)((MM_GATHER_PREFETCH ? cur_e1 : a.rp[i + 1]) - e0);
             const int32_t* __restrict__ colr = a.col + e0;
             const float* __restrict__ dr = a.d + e0;
             const float* __restrict__ wr = a.w + e0;
@@ -145,7 +168,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 // Eq.(3) excludes the own representative H(i); kernel (c)
                 // summed all k, so its term goes into C (subtracted), computed with
                 // kernel (c)'s hi/lo differencing (Q25)
-                int32_t h = __ldg(a.anc + i);
+                int32_t h = MM_GATHER_PREFETCH ? cur_anc : __ldg(a.anc + i);
                 if (a.rpos != nullptr) h = __ldg(a.rpos + h);
                 const float4 rh = __ldg(a.rep_hi + h), rl = __ldg(a.rep_lo + h);
                 const float4 fr = a.frame != nullptr ? __ldg(a.frame) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -163,7 +186,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 if constexpr (DIM == 3) C.z = fmaf(dz, inv, C.z);
             }
             if (a.parent != nullptr) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
-                const int32_t p = __ldg(a.parent + i);
+                const int32_t p = MM_GATHER_PREFETCH ? cur_par : __ldg(a.parent + i);
                 const int32_t c0 = __ldg(a.child_ptr + p), c1 = __ldg(a.child_ptr + p + 1);
                 for (int32_t c = c0 + lg; c < c1; c += G) {
                     const int32_t j = __ldg(a.child + c);
