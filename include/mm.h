@@ -24,6 +24,11 @@
  *   - STREAMS: every call enqueues on `stream` (a cudaStream_t; NULL = legacy
  *     default stream).  Calls marked "async" do not synchronise the host;
  *     calls marked "syncs" synchronise `stream` before returning.
+ *   - THREADS: every entry point may be called from several host threads at
+ *     once.  mm_layout, mm_layout_schedule and mm_build_hierarchy(_sclap) use
+ *     device-resident grid-barrier / schedule state, so the library runs them
+ *     one at a time per process (a lock held from their first launch to their
+ *     final stream synchronisation); the other calls are not serialised.
  *   - ERRORS: argument checks are synchronous and happen before any launch;
  *     on error nothing is enqueued and mm_last_error() holds a thread-local
  *     message.  Device-detected problems (non-finite coordinates) are written

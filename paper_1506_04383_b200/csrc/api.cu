@@ -702,9 +702,18 @@ struct HierMode {
     double f0 = 20.0, b = 2.0;
 };
 
+// Calls that drive the device-resident synchronisation state (the grid
+// barriers of k_match_level and k_small_level, the schedule loop's
+// g_sched_state) hold this lock from their first launch until their final
+// stream synchronisation, so concurrent calls from several host threads (any
+// streams) cannot interleave on that state.  Recursive: mm_layout builds its
+// hierarchy through build_hierarchy_impl.
+std::recursive_mutex g_state_mu;
+
 mm_status build_hierarchy_impl(const mm_graph* g, const int32_t* c, int dim, uint64_t seed, int32_t n_stop,
                                int32_t max_levels, int32_t max_rounds, mm_hierarchy** out, cudaStream_t st,
                                const HierMode& mode = HierMode()) {
+    std::lock_guard<std::recursive_mutex> state_lock(g_state_mu);
     const int32_t n0 = g->n;
     const int64_t nnz0 = g->nnz;
     mm_hierarchy* H = new mm_hierarchy();
@@ -1529,13 +1538,17 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
     const int st_w = stride_of(dim);
     const size_t xbytes = (size_t)n0 * st_w * sizeof(float);
     cudaEvent_t ev = nullptr;
-    // the driver's own non-blocking stream (persistent, so that stream-ordered
-    // workspace reuse and the graph cache see the same addresses call after call)
-    static std::mutex s_stream_mu;
-    static cudaStream_t s_ls = nullptr;
-    std::lock_guard<std::mutex> stream_lock(s_stream_mu);
-    if (!s_ls) MM_CU(cudaStreamCreateWithFlags(&s_ls, cudaStreamNonBlocking), "mm_layout stream");
-    cudaStream_t ls = s_ls;
+    // the driver's own non-blocking stream per device (persistent, so that
+    // stream-ordered workspace reuse and the graph cache see the same addresses
+    // call after call); the state lock serialises layouts (see g_state_mu)
+    constexpr int kMaxDevices = 64;
+    static cudaStream_t s_ls[kMaxDevices] = {};
+    std::lock_guard<std::recursive_mutex> state_lock(g_state_mu);
+    int dev = 0;
+    MM_CU(cudaGetDevice(&dev), "mm_layout device");
+    if (dev < 0 || dev >= kMaxDevices) { set_err("%s: device ordinal %d >= %d", who, dev, kMaxDevices); return MM_ERR_UNSUPPORTED; }
+    if (!s_ls[dev]) MM_CU(cudaStreamCreateWithFlags(&s_ls[dev], cudaStreamNonBlocking), "mm_layout stream");
+    cudaStream_t ls = s_ls[dev];
     struct StreamGuard {
         cudaStream_t s;
         cudaEvent_t e;

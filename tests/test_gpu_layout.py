@@ -166,3 +166,56 @@ def test_layout_bitwise_deterministic(mm):
     xs2, r2 = mm.layout_schedule(g, S, 2, 0.0, 2, mm.paper_schedule(max_final_iters=5), w.seed, n_stop=200,
                                  sclap=True, disc=True)
     assert np.array_equal(s1, xs2.cpu().numpy()) and r1["sweeps_level"] == r2["sweeps_level"]
+
+
+def test_concurrent_calls_from_threads(mm):
+    """Layouts and hierarchy builds issued at the same time from several host
+    threads, each on its own stream, give bitwise the results of the same calls
+    made one after another: the device-resident barrier and schedule state
+    (k_match_level, k_small_level, the schedule loop) is held by one call at a
+    time (g_state_mu in api.cu)."""
+    import threading
+
+    import torch
+
+    wa, wb = workload("cfg3_mesh64"), workload("cfg1_grid16")
+    ga, Sa = mm.graph_to_device(wa.graph), mm.sset_to_device(wa.S)
+    gb, Sb = mm.graph_to_device(wb.graph), mm.sset_to_device(wb.S)
+
+    def run_a():
+        x, r = mm.layout_schedule(ga, Sa, 2, 0.0, 2, mm.paper_schedule(max_final_iters=5), wa.seed, n_stop=200)
+        return x.cpu().numpy().copy(), r["energy"]
+
+    def run_b():
+        x, r = mm.layout(gb, Sb, 2, wb.alpha, wb.q, 2, [8], wb.seed, n_stop=20)
+        return x.cpu().numpy().copy(), r["energy"]
+
+    def run_h():
+        h = mm.build_hierarchy(ga, 2, 7, n_stop=50)
+        return [h.level_host(l)["parent"].copy() for l in range(h.num_levels - 1)]
+
+    ref = {"a": run_a(), "b": run_b(), "h": run_h()}
+    fns = {"a": run_a, "b": run_b, "h": run_h}
+    out, errs = {}, []
+
+    def worker(key):
+        try:
+            s = torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    out[(key, rep)] = fns[key]()
+                s.synchronize()
+        except Exception as e:  # surfaced below
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=worker, args=(k,)) for k in ("a", "b", "h", "a", "b")]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for (key, rep), v in out.items():
+        if key == "h":
+            assert len(v) == len(ref["h"]) and all(np.array_equal(p, q) for p, q in zip(v, ref["h"]))
+        else:
+            assert np.array_equal(v[0], ref[key][0]) and v[1] == ref[key][1], (key, rep)
