@@ -99,9 +99,11 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
         float4 R = make_float4(0.f, 0.f, 0.f, 0.f);
         if (valid) {
             xi = load_x<DIM>(a.x, i);
-            if (lg == 0) {
+            {
                 // repulsion partials of this vertex (static schedule slots), fetched
-                // first so that their latency overlaps the S-row loads
+                // first so that their latency overlaps the S-row loads; the slots
+                // and j-side rows are split over the group's lanes (lane lg takes
+                // every G-th, in increasing order) and combined by the group sum below
                 const int stride = DIM == 2 ? 2 : 4;
                 // kernel (c) processes targets by slot (spatial order, Q27): the slot
                 // count follows the slot's block; the partials sit at the vertex id
@@ -112,7 +114,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                                   sched_first_cta_tri(tri_prefix((int32_t)tb, a.tri), a.tri) + 1
                             : sched_first_cta((tb + 1) * a.sch.Ub - 1, a.sch) -
                                   sched_first_cta(tb * a.sch.Ub, a.sch) + 1;
-                for (int p = 0; p < nslot; ++p) {
+                for (int p = lg; p < nslot; p += G) {
                     const float4 v = load_x<DIM>(a.part + (int64_t)p * a.n * stride, i);
                     R.x += v.x;
                     R.y += v.y;
@@ -120,7 +122,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 }
                 // symmetric mode: j-side sums of the block pairs (I, tb), I < tb
                 if (a.jpart) {
-                    for (int64_t I = 0; I < tb; ++I) {
+                    for (int64_t I = lg; I < tb; I += G) {
                         const float4 v = load_x<DIM>(a.jpart + I * a.n * stride, i);
                         R.x += v.x;
                         R.y += v.y;
@@ -201,9 +203,12 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
         A.y = group_sum<G>(A.y);
         C.x = group_sum<G>(C.x);
         C.y = group_sum<G>(C.y);
+        R.x = group_sum<G>(R.x);
+        R.y = group_sum<G>(R.y);
         if constexpr (DIM == 3) {
             A.z = group_sum<G>(A.z);
             C.z = group_sum<G>(C.z);
+            R.z = group_sum<G>(R.z);
         }
         if (valid && lg == 0) {
             R.x -= C.x;
@@ -388,8 +393,11 @@ int pick_group(double mean_row) {
 
 }  // namespace
 
-int gather_blocks(int32_t n, double mean_row) {
-    const int G = pick_group(mean_row);
+#ifndef MM_GATHER_SYM_GMIN
+#define MM_GATHER_SYM_GMIN 1  // lanes per vertex at least, after the symmetric kernel (b); 4 / 8 / 16 measured slower at cfg2 (tools/gpu_session85.sh)
+#endif
+
+static int gather_blocks_g(int32_t n, int G) {
     const int64_t need = ((int64_t)n * G + kGBlock - 1) / kGBlock;
     static const int cap = [] {
         int dev = 0, sms = 148, occ = 0;
@@ -404,9 +412,14 @@ int gather_blocks(int32_t n, double mean_row) {
     return (int)std::max<int64_t>(1, std::min<int64_t>(need, cap));
 }
 
+int gather_blocks(int32_t n, double mean_row) { return gather_blocks_g(n, pick_group(mean_row)); }
+
 cudaError_t launch_gather(int dim, const GatherArgs& a, double mean_row, cudaStream_t st) {
-    const int G = pick_group(mean_row);
-    const int nb = gather_blocks(a.n, mean_row);
+    int G = pick_group(mean_row);
+    // after the symmetric exact kernel a vertex of block b sums b j-side rows
+    // (about n / 2048 on average) besides its slots: spread them over more lanes
+    if (a.jpart != nullptr) G = std::max(G, MM_GATHER_SYM_GMIN);
+    const int nb = gather_blocks_g(a.n, G);
     const float cexp = -(a.q + 2.0f) * 0.5f;
     const bool qpow = a.q != 0.0f;
     LaunchScope ls("gather_update", st);
