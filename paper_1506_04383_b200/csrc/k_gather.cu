@@ -62,6 +62,9 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
 #define MM_GATHER_UNROLL 4
 #endif
 constexpr int kGatherUnroll = MM_GATHER_UNROLL;
+#ifndef MM_GATHER_UNROLL_G1
+#define MM_GATHER_UNROLL_G1 2  // one lane per vertex (short rows, e.g. cfg5's 6): unroll 2 measured +10% there (tools/gpu_session87.sh)
+#endif
 template <int DIM, bool QPOW, int G>
 __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a, float cexp) {
     if (a.alpha_dev) a.alpha = (float)*a.alpha_dev;  // same rounding as the host path's (float)alpha
@@ -137,7 +140,8 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
             const int32_t* __restrict__ colr = a.col + e0;
             const float* __restrict__ dr = a.d + e0;
             const float* __restrict__ wr = a.w + e0;
-#pragma unroll kGatherUnroll
+            constexpr int kUnr = G == 1 ? MM_GATHER_UNROLL_G1 : kGatherUnroll;
+#pragma unroll kUnr
             for (int k = lg; k < len; k += G) {
                 const int32_t j = __ldcs(colr + k);
                 const float dd = __ldcs(dr + k), ww = __ldcs(wr + k);
