@@ -62,6 +62,9 @@ __device__ __forceinline__ void r_value(const float4& xi, const float4& xj, floa
 #define MM_GATHER_UNROLL 4
 #endif
 constexpr int kGatherUnroll = MM_GATHER_UNROLL;
+#ifndef MM_GATHER_SLOAD
+#define MM_GATHER_SLOAD 1  // S rows through the normal (L2-retaining) path; 0: evict-first streaming (measured slower: cfg5 0.105 vs 0.093 ms, cfg3 0.036 vs 0.031 ms; tools/gpu_session89.sh)
+#endif
 #ifndef MM_GATHER_UNROLL_G1
 #define MM_GATHER_UNROLL_G1 2  // one lane per vertex (short rows, e.g. cfg5's 6): unroll 2 measured +10% there (tools/gpu_session87.sh)
 #endif
@@ -134,7 +137,8 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 }
             }
             // row i: 64-bit base, 32-bit offsets; the S arrays are read once per
-            // sweep (streaming loads, evict-first) so that x stays in L2
+            // sweep through the normal cached path (what fits of them stays in
+            // the 126 MB L2 for the next sweep: cfg3's 60 MB, most of cfg5's 150 MB)
             const int64_t e0 = MM_GATHER_PREFETCH ? cur_e0 : a.rp[i];
             const int len = (int)((MM_GATHER_PREFETCH ? cur_e1 : a.rp[i + 1]) - e0);
             const int32_t* __restrict__ colr = a.col + e0;
@@ -143,8 +147,13 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
             constexpr int kUnr = G == 1 ? MM_GATHER_UNROLL_G1 : kGatherUnroll;
 #pragma unroll kUnr
             for (int k = lg; k < len; k += G) {
+#if MM_GATHER_SLOAD
+                const int32_t j = __ldg(colr + k);
+                const float dd = __ldg(dr + k), ww = __ldg(wr + k);
+#else
                 const int32_t j = __ldcs(colr + k);
                 const float dd = __ldcs(dr + k), ww = __ldcs(wr + k);
+#endif
                 const float4 xj = load_x<DIM>(a.x, j);
                 const float dx = xi.x - xj.x, dy = xi.y - xj.y;
                 float r2 = fmaf(dx, dx, kEps2);
