@@ -344,15 +344,18 @@ def run_gpu(args):
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
         hosts = [pin(w.S.row_ptr.astype(np.int64)), pin(w.S.col.astype(np.int32)),
                  pin(w.S.d.astype(np.float32)), pin(w.S.w.astype(np.float32))]
-        if w.h == 0:
-            hosts.append(pin(mm.coords_layout(w.x0)))
-        else:
+        # exactly the arrays the timed call consumes: the graph when the hierarchy is
+        # built (multilevel or --schedule), the start layout for single-level exact runs
+        need_graph = w.h > 0 or args.schedule
+        if need_graph:
             hosts += [pin(w.graph.row_ptr.astype(np.int64)), pin(w.graph.col.astype(np.int32))]
+        else:
+            hosts.append(pin(mm.coords_layout(w.x0)))
         devs = [torch.empty_like(h, device=dev) for h in hosts]
         h_out = torch.empty(tuple(out.shape), dtype=torch.float32).pin_memory()
         Se = mm.DeviceSSet(*devs[:4])
-        Ge = mm.DeviceGraph(devs[4], devs[5]) if w.h > 0 else None
-        xe = devs[4] if w.h == 0 else None
+        Ge = mm.DeviceGraph(devs[4], devs[5]) if need_graph else None
+        xe = None if need_graph else devs[4]
         h2d = sum(t.numel() * t.element_size() for t in hosts)
         d2h = h_out.numel() * h_out.element_size() + 3 * 8  # layout + (stress, entropy, energy)
 
@@ -360,7 +363,7 @@ def run_gpu(args):
             for hd, dd in zip(hosts, devs):
                 dd.copy_(hd, non_blocking=True)
             if args.schedule:
-                y, r = mm.layout_schedule(G, Se, w.dim, w.q, args.h, sched, w.seed, out=out)
+                y, r = mm.layout_schedule(Ge, Se, w.dim, w.q, args.h, sched, w.seed, out=out)
             else:
                 y, r = mm.layout(Ge, Se, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=xe, out=out)
             h_out.copy_(y, non_blocking=True)

@@ -178,8 +178,8 @@ MM_API mm_status mm_sweep_workspace(int32_t n, int dim, const mm_approx* ap, siz
  * (q = 0 is the paper's r-value).  The representatives are the
  * unweighted means of x_in over each H class (Q11/Q12).
  * x_out must not alias x_in.  ws/ws_bytes: caller scratch of at least
- * mm_sweep_workspace() bytes, or NULL/0 to let the library allocate it
- * stream-ordered.  stats (device, nullable) receives mm_sweep_stats.  async.
+ * mm_sweep_workspace() bytes, 256-B aligned (else MM_ERR_INVALID_ARGUMENT),
+ * or NULL/0 to let the library allocate it stream-ordered.  stats (device, nullable) receives mm_sweep_stats.  async.
  * Eq.(3) evaluation order (results equal up to FP32 rounding, DESIGN.md
  * Q26-Q28): targets and representatives are visited in spatial order and
  * representatives grouped by mass; tiles far from a warp's targets drop the
@@ -191,12 +191,28 @@ MM_API mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const
                    const float* x_in, float* x_out, mm_sweep_stats* stats,
                    void* ws, size_t ws_bytes, mm_stream_t stream);
 
+/* K Jacobi sweeps ("a single update step of the coordinates of all
+ * vertices using Eq.(2)" per iteration; "the current iteration uses the
+ * coordinates that have been computed in the previous iteration"), each one
+ * what mm_sweep computes, from x_in to x_out (must not alias).  With ap the
+ * representatives are refreshed before every sweep (Q12).  A level that
+ * qualifies (n <= 32,768 for Eq.(3), <= 4,096 exact; MM_SMALL_N caps it)
+ * runs all K sweeps in the persistent small-level kernel, as mm_layout does;
+ * otherwise the K sweeps are one CUDA graph of the tiled kernels.
+ * stats (device, nullable) receives the LAST sweep's mm_sweep_stats.  K = 0
+ * copies.  Returns MM_ERR_NONFINITE if a non-finite coordinate appeared.
+ * syncs `stream` (and serialises with mm_layout like it). */
+MM_API mm_status mm_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap,
+                           const float* x_in, float* x_out, int32_t K, mm_sweep_stats* stats, mm_stream_t stream);
+
 /* Maxent-stress energy Eq.(1) in the S form with readings Q3/Q4:
  * out[0] = stress = 1/2 sum_i sum_{j in S_i} w (|x_i-x_j| - d)^2
  * out[1] = entropy = 1/2 sum_i sum_{j notin S_i, j != i} phi_q(|x_i - x_j|),
  *          phi_0(r) = -ln r, phi_q(r) = r^-q / q
  * out[2] = stress + alpha * entropy.  out is HOST double[3].
- * FP32 per pair, FP64 accumulation, fixed summation order (deterministic).
+ * FP32 per pair, FP64 accumulation, fixed summation order (deterministic):
+ * the per-CTA FP64 partials are copied to the host and summed there in CTA
+ * order (a few thousand doubles; this is part of the sync, not a fallback).
  * A coincident non-S pair returns MM_ERR_NONFINITE.  syncs. */
 MM_API mm_status mm_energy(const mm_sset* S, int dim, double alpha, double q, const float* x,
                     double* out, mm_stream_t stream);
@@ -232,6 +248,19 @@ MM_API void mm_hierarchy_free(mm_hierarchy* h);
 MM_API mm_status mm_hierarchy_copy_level(const mm_hierarchy* h, int32_t level, int64_t* row_ptr, int32_t* col,
                                          int32_t* omega, int32_t* c, int32_t* parent, float* d, float* w,
                                          mm_stream_t stream);
+
+/* Prolongation of one level (the step mm_layout runs between levels):
+ * x[u] = xc[parent[u]] + delta_u for u < n_fine.
+ *   c_coarse == NULL: reading Q15 (BASELINE.json configs[2]): delta_u,k =
+ *     1e-3 (2 U - 1), U = the counter RNG of (seed, jitter tag, level, u, k).
+ *   c_coarse != NULL: the paper's disc (reading R7): angle 2 pi U0,
+ *     distance c(parent)^(1/dim) U1 (dim 3: direction from z = 2 U2 - 1).
+ * parent: device int32[n_fine] (ids < the coarse level's size, not checked);
+ * xc: device coarse coordinates; c_coarse: device int32 coarse node weights;
+ * x: device output [n_fine] in the coordinate layout (must not alias xc).
+ * level = the FINE level's index (the RNG key).  async. */
+MM_API mm_status mm_prolong(int32_t n_fine, int dim, const int32_t* parent, const float* xc,
+                            const int32_t* c_coarse, uint64_t seed, int32_t level, float* x, mm_stream_t stream);
 
 /* Multilevel layout.  h = 0: single level, x_init (device, required) is
  * iterated sweeps[0] exact sweeps (Eq.(2)).  h > 0: hierarchy (n_stop, seed),

@@ -15,6 +15,8 @@ Parity status per function:
   build_hierarchy  pinned (P11 invariants, brute-force contraction, hand instances)
   centroids        pinned (P12 independent recomputation)
   prolong/init     pinned (P13 bounds; RNG pinned to SplitMix64's published vector)
+  prolong_disc     pinned (radius <= c^(1/dim); distance / r uniform on [0, 1] and
+                   angle / direction uniform, the laws P:242 states; RNG keys)
   layout           parity unpinned by the paper for full multilevel trajectories
                    (Q20); its pieces are pinned individually.
 """
@@ -100,6 +102,7 @@ def lib() -> ctypes.CDLL:
     L.or_coarse_sset.argtypes = [c_i32, c_i64, _i64p, _i32p, _i64p, c_int, _f64p, _f64p]
     L.or_init_box.argtypes = [c_i32, c_int, c_dbl, c_u64, c_i32, _f64p]
     L.or_prolong.argtypes = [c_i32, c_int, _i32p, _f64p, c_u64, c_i32, _f64p]
+    L.or_prolong_disc.argtypes = [c_i32, c_int, _i32p, _f64p, _i64p, c_u64, c_i32, _f64p]
     L.or_layout.argtypes = [c_i32, c_int, _i64p, _i32p, _i64p, _i32p, _f64p, _f64p, c_dbl, c_dbl, c_int,
                             _i32p, c_i32, c_u64, c_i32, _f64p, _f64p, _f64p, _i32p, c_int]
     L.or_layout_schedule.argtypes = [c_i32, c_int, _i64p, _i32p, _i64p, _i32p, _f64p, _f64p, c_dbl, c_int,
@@ -318,6 +321,19 @@ def prolong(parent: np.ndarray, xc: np.ndarray, seed: int, level: int) -> np.nda
     x = np.empty((n, dim), dtype=np.float64)
     _check(lib().or_prolong(n, dim, _p(parent, ctypes.c_int32), _p(xc, ctypes.c_double), seed, level,
                             _p(x, ctypes.c_double)), "prolong")
+    return x
+
+
+def prolong_disc(parent: np.ndarray, xc: np.ndarray, c_coarse: np.ndarray, seed: int, level: int) -> np.ndarray:
+    """The paper's disc prolongation (reading R7): angle 2 pi U0,
+    distance c(parent)^(1/dim) U1 (dim 3: direction from z = 2 U2 - 1)."""
+    parent = np.ascontiguousarray(parent, dtype=np.int32)
+    xc = np.ascontiguousarray(xc, dtype=np.float64)
+    cc = np.ascontiguousarray(c_coarse, dtype=np.int64)
+    n, dim = parent.shape[0], xc.shape[1]
+    x = np.empty((n, dim), dtype=np.float64)
+    _check(lib().or_prolong_disc(n, dim, _p(parent, ctypes.c_int32), _p(xc, ctypes.c_double),
+                                 _p(cc, ctypes.c_int64), seed, level, _p(x, ctypes.c_double)), "prolong_disc")
     return x
 
 

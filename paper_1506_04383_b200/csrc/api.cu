@@ -581,6 +581,10 @@ mm_status mm_sweep(const mm_sset* S, int dim, float alpha, float q, const mm_app
         set_err("mm_sweep: workspace too small (%zu < %zu B)", ws_bytes, need);
         return MM_ERR_INVALID_ARGUMENT;
     }
+    if (ws && ((uintptr_t)ws & 255u) != 0) {
+        set_err("mm_sweep: workspace must be 256-B aligned (got %p)", ws);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
     Carver cv(base, cap);
     SweepBufs sb;
     if (!carve_sweep(cv, n, dim, ap ? ap->k : 0, ap != nullptr, mean_row, sb)) {
@@ -1770,6 +1774,63 @@ extern "C" mm_status mm_layout(const mm_graph* g, const mm_sset* S, int dim, flo
                        (cudaStream_t)stream, "mm_layout");
 }
 
+extern "C" mm_status mm_sweeps(const mm_sset* S, int dim, float alpha, float q, const mm_approx* ap,
+                               const float* x_in, float* x_out, int32_t K, mm_sweep_stats* stats,
+                               mm_stream_t stream) {
+    mm_status s;
+    const char* who = "mm_sweeps";
+    if ((s = check_sset(S, who)) != MM_OK) return s;
+    if ((s = check_dim_q(dim, q, who)) != MM_OK) return s;
+    if ((s = check_x(x_in, dim, "x_in", who)) != MM_OK) return s;
+    if ((s = check_x(x_out, dim, "x_out", who)) != MM_OK) return s;
+    const int32_t n = S->n;
+    const size_t xbytes = (size_t)n * stride_of(dim) * sizeof(float);
+    const char *a0 = (const char*)x_in, *b0 = (const char*)x_out;
+    if (a0 < b0 + xbytes && b0 < a0 + xbytes) { set_err("%s: x_out must not alias x_in", who); return MM_ERR_INVALID_ARGUMENT; }
+    if (K < 0 || !isfinite(alpha)) { set_err("%s: K >= 0 and a finite alpha required", who); return MM_ERR_INVALID_ARGUMENT; }
+    if (ap && (ap->k <= 0 || ap->k > n || !ap->parent || !ap->ancestor)) {
+        set_err("%s: bad mm_approx (k=%d must be in [1, n], maps non-NULL)", who, ap->k);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    // the persistent small-level kernel keeps its grid-barrier state in device symbols
+    std::lock_guard<std::recursive_mutex> state_lock(g_state_mu);
+    const double mean_row = (double)S->nnz / (double)n;
+    const size_t need = sweep_bytes(n, dim, ap ? ap->k : 0, ap != nullptr, mean_row) + al(xbytes) +
+                        al(sizeof(mm_sweep_stats));
+    DevBuf buf(need, st);
+    if (!buf.p) { set_err("%s: out of device memory (%zu B)", who, need); return MM_ERR_OUT_OF_MEMORY; }
+    Carver cv(buf.p, need);
+    float* tmpx = cv.take<float>(xbytes / sizeof(float));
+    mm_sweep_stats* dstats = cv.take<mm_sweep_stats>(1);
+    SweepBufs sb;
+    if (!carve_sweep(cv, n, dim, ap ? ap->k : 0, ap != nullptr, mean_row, sb)) {
+        set_err("%s: carving failed", who);
+        return MM_ERR_INVALID_ARGUMENT;
+    }
+    MM_CU(cudaMemsetAsync(sb.flags, 0, 4 * sizeof(int32_t), st), "mm_sweeps memset");
+    MM_CU(cudaMemsetAsync(dstats, 0, sizeof(mm_sweep_stats), st), "mm_sweeps memset");
+    const float* res = x_in;
+    if (K > 0) {
+        if (ap) MM_CU(prepare_approx(n, dim, ap, x_in, sb, st), "mm_sweeps prepare_approx");
+        int32_t nsw = 0;
+        s = MM_ERR_UNSUPPORTED;
+        if (small_level_ok(dim, n, ap ? ap->k : 0, ap != nullptr))
+            s = run_small(S, dim, q, ap, x_in, x_out, tmpx, dstats, sb, st, 0, K, alpha, nullptr, &res, &nsw);
+        if (s == MM_ERR_UNSUPPORTED)
+            MM_CU(run_sweeps(S, dim, alpha, q, ap, x_in, x_out, tmpx, K, dstats, sb, st, &res), "mm_sweeps");
+        else if (s != MM_OK)
+            return s;
+    }
+    if (res != x_out) MM_CU(cudaMemcpyAsync(x_out, res, xbytes, cudaMemcpyDeviceToDevice, st), "mm_sweeps copy");
+    if (stats) MM_CU(cudaMemcpyAsync(stats, dstats, sizeof(mm_sweep_stats), cudaMemcpyDeviceToDevice, st), "mm_sweeps stats");
+    mm_sweep_stats hs;
+    MM_CU(cudaMemcpyAsync(&hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, st), "mm_sweeps d2h");
+    MM_CU(cudaStreamSynchronize(st), "mm_sweeps sync");
+    if (hs.flags & 1) { set_err("%s: non-finite coordinate produced", who); return MM_ERR_NONFINITE; }
+    return MM_OK;
+}
+
 extern "C" mm_status mm_layout_schedule(const mm_graph* g, const mm_sset* S, int dim, float q, int h,
                                         const mm_schedule* sch, uint64_t seed, int32_t n_stop, int32_t flags,
                                         const float* x_init, float* x_out, mm_layout_report* rep, mm_stream_t stream) {
@@ -1835,6 +1896,23 @@ extern "C" mm_status mm_full_stress(const mm_graph* g, int dim, const float* x, 
     out[1] = sc;
     out[2] = sc * sc * B - 2.0 * sc * A + C;
     out[3] = P;
+    return MM_OK;
+}
+
+// ================================================================== prolongation
+extern "C" mm_status mm_prolong(int32_t n_fine, int dim, const int32_t* parent, const float* xc,
+                                const int32_t* c_coarse, uint64_t seed, int32_t level, float* x, mm_stream_t stream) {
+    mm_status s;
+    if (n_fine < 0) { set_err("mm_prolong: n_fine < 0"); return MM_ERR_INVALID_ARGUMENT; }
+    if (dim != 2 && dim != 3) { set_err("mm_prolong: dim must be 2 or 3 (got %d)", dim); return MM_ERR_UNSUPPORTED; }
+    if (n_fine == 0) return MM_OK;
+    if (!parent) { set_err("mm_prolong: parent is NULL"); return MM_ERR_INVALID_ARGUMENT; }
+    if ((s = check_x(xc, dim, "xc", "mm_prolong")) != MM_OK) return s;
+    if ((s = check_x(x, dim, "x", "mm_prolong")) != MM_OK) return s;
+    if (x == xc) { set_err("mm_prolong: x must not alias xc"); return MM_ERR_INVALID_ARGUMENT; }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c_coarse) MM_CU(launch_prolong_disc(dim, n_fine, parent, xc, c_coarse, seed, level, x, st), "mm_prolong");
+    else MM_CU(launch_prolong(dim, n_fine, parent, xc, seed, level, x, st), "mm_prolong");
     return MM_OK;
 }
 

@@ -22,7 +22,7 @@ MM_ERR_OUT_OF_MEMORY, MM_ERR_CUDA, MM_ERR_UNSUPPORTED = -4, -5, -6
 MM_MAX_LEVELS = 64
 
 EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator", "mm_validate_sset",
-           "mm_sweep_workspace",
+           "mm_sweep_workspace", "mm_prolong", "mm_sweeps",
            "mm_sweep", "mm_energy", "mm_build_hierarchy", "mm_build_hierarchy_sclap", "mm_hierarchy_num_levels", "mm_hierarchy_level",
            "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_full_stress",
            "mm_launch_count", "mm_exact_kernel_variant",
@@ -109,6 +109,10 @@ def load() -> ctypes.CDLL:
     L.mm_version.argtypes = []; L.mm_version.restype = ctypes.c_char_p
     L.mm_set_allocator.argtypes = [vp, vp, vp]; L.mm_set_allocator.restype = ctypes.c_int
     L.mm_validate_sset.argtypes = [P(mm_sset), vp]; L.mm_validate_sset.restype = ctypes.c_int
+    L.mm_sweeps.argtypes = [P(mm_sset), ctypes.c_int, f32, f32, P(mm_approx), vp, vp, i32, vp, vp]
+    L.mm_sweeps.restype = ctypes.c_int
+    L.mm_prolong.argtypes = [i32, ctypes.c_int, vp, vp, vp, u64, i32, vp, vp]
+    L.mm_prolong.restype = ctypes.c_int
     L.mm_sweep_workspace.argtypes = [i32, ctypes.c_int, P(mm_approx), P(ctypes.c_size_t)]
     L.mm_sweep_workspace.restype = ctypes.c_int
     L.mm_sweep.argtypes = [P(mm_sset), ctypes.c_int, f32, f32, P(mm_approx), vp, vp, vp, vp, ctypes.c_size_t, vp]
@@ -276,6 +280,27 @@ def sweep(S: DeviceSSet, x, alpha: float, q: float, parent=None, ancestor=None, 
     return out
 
 
+def sweeps(S: DeviceSSet, x, alpha: float, q: float, K: int, parent=None, ancestor=None, k: int = 0,
+           out=None, stats: bool = False):
+    """mm_sweeps: K Jacobi sweeps (Eq.(2), or Eq.(3) with parent/ancestor/k)
+    from x; small levels run in the persistent kernel as in mm_layout."""
+    torch = _torch()
+    dim = _dim_of(x)
+    if out is None:
+        out = torch.empty_like(x)
+    st = torch.zeros(4, dtype=torch.float64, device=x.device) if stats else None
+    ap = mm_approx(int(k), _ptr(parent), _ptr(ancestor)) if parent is not None else None
+    s = S.c_struct()
+    rc = load().mm_sweeps(ctypes.byref(s), dim, float(alpha), float(q), ctypes.byref(ap) if ap else None,
+                          _ptr(x), _ptr(out), int(K), _ptr(st), _stream_ptr(x.device))
+    _check(rc, "mm_sweeps")
+    if stats:
+        h = st.cpu().numpy()
+        flags = int(np.frombuffer(h[3:4].tobytes(), dtype=np.int32)[0])
+        return out, {"dx2": float(h[0]), "x2": float(h[1]), "stress": float(h[2]), "flags": flags}
+    return out
+
+
 def energy(S: DeviceSSet, x, alpha: float, q: float):
     """Maxent-stress energy Eq.(1): (stress, entropy, total)."""
     L = load()
@@ -430,6 +455,21 @@ def full_stress(g: DeviceGraph, x):
     gs = g.c_struct()
     _check(L.mm_full_stress(ctypes.byref(gs), _dim_of(x), _ptr(x), out, _stream_ptr(x.device)), "mm_full_stress")
     return float(out[0]), float(out[1]), float(out[2]), int(out[3])
+
+
+def prolong(parent, xc, seed: int, level: int, c_coarse=None, out=None):
+    """mm_prolong: x[u] = xc[parent[u]] + jitter (Q15) or the paper's disc
+     when the coarse node weights c_coarse are given.  parent: CUDA
+    int32 (n_fine,); xc: CUDA float32 coarse coordinates; level: the fine level."""
+    torch = _torch()
+    dim = _dim_of(xc)
+    n = int(parent.shape[0])
+    if out is None:
+        out = torch.empty((n, xc.shape[1]), dtype=torch.float32, device=xc.device)
+    rc = load().mm_prolong(n, dim, _ptr(parent), _ptr(xc), _ptr(c_coarse), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                           int(level), _ptr(out), _stream_ptr(xc.device))
+    _check(rc, "mm_prolong")
+    return out
 
 
 def validate_sset(S: DeviceSSet):

@@ -10,7 +10,7 @@ import pytest
 
 import oracle
 from tests import helpers as H
-from tests.gpu_common import ENERGY_TOL, assert_energy_or_chaos, workload
+from tests.gpu_common import ENERGY_TOL, assert_energy, workload
 from workloads import configs
 
 pytestmark = pytest.mark.gpu
@@ -105,7 +105,7 @@ def test_layout_exact_cfg1_full_run(mm):
     S = mm.sset_to_device(w.S)
     x, rep = mm.layout(None, S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=mm.coords_to_device(w.x0))
     xo, eo, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=w.x0.astype(np.float64))
-    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep, eo)
+    assert_energy(rep["energy"], eo[2], "layout cfg1")
     # isolate kernel error from trajectory divergence: oracle energy of the GPU layout
     eg = oracle.energy(w.S, mm.coords_from_device(x, 2), w.alpha, w.q)
     assert _rel(rep["energy"], eg[2]) <= 1e-4
@@ -117,7 +117,7 @@ def test_layout_exact_rgg_full_run(mm):
     S = mm.sset_to_device(w.S)
     x, rep = mm.layout(None, S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=mm.coords_to_device(w.x0))
     xo, eo, _ = oracle.layout(w.graph, w.S, 2, w.alpha, w.q, 0, [w.sweeps], w.seed, x_init=w.x0.astype(np.float64))
-    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep, eo)
+    assert_energy(rep["energy"], eo[2], "layout cfg2_rgg4096")
 
 
 @pytest.mark.parametrize("name,n_stop", [("cfg3_mesh64", 200), ("cfg5_grid16", 200), ("cfg4_cl20000", 1000),
@@ -134,11 +134,8 @@ def test_layout_multilevel_full_run(mm, name, n_stop):
     eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), w.alpha, w.q)
     assert _rel(rep["energy"], eg[2]) <= 1e-4, (rep["energy"], eg)
 
-    def control(s):
-        return oracle.layout(w.graph, w.S, w.dim, w.alpha * (1 + s), w.q, w.h, [w.sweeps], w.seed,
-                             n_stop=n_stop)[1][2]
-
-    assert_energy_or_chaos(rep["energy"], eo[2], control, name)
+    assert_energy(rep["energy"], eo[2], f"layout {name} n_stop={n_stop}", levels=nl,
+                  rel_kernel=_rel(rep["energy"], eg[2]))
 
 
 def test_layout_in_place(mm):

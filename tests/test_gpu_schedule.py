@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle
-from tests.gpu_common import ENERGY_TOL, assert_energy_or_chaos, workload
+from tests.gpu_common import assert_energy, workload
 from workloads import dynamic, sset
 
 pytestmark = pytest.mark.gpu
@@ -42,7 +42,7 @@ def test_single_level_schedule(mm, name, cap):
     xo, eo, nl, sw = oracle.layout_schedule(w.graph, w.S, 2, w.q, 0, os_, w.seed, multilevel=False,
                                             x_init=w.x0.astype(np.float64))
     assert rep["sweeps_level"] == list(sw), (rep["sweeps_level"], list(sw))
-    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep["energy"], eo)
+    assert_energy(rep["energy"], eo[2], f"schedule {name} single-level")
 
 
 @pytest.mark.parametrize("name,h,n_stop,cap", [("cfg3_mesh32", 0, 100, 25), ("cfg3_mesh64", 2, 200, 25),
@@ -57,12 +57,8 @@ def test_multilevel_schedule(mm, name, h, n_stop, cap):
     eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), 0.008, w.q)
     assert _rel(rep["energy"], eg[2]) <= 1e-4
     assert rep["sweeps_level"] == list(sw), (rep["sweeps_level"], list(sw))
-
-    def control(s):
-        ps = oracle.paper_schedule(max_final_iters=cap, alpha0=1.0 * (1 + s), alpha_min=0.008 * (1 + s))
-        return oracle.layout_schedule(w.graph, w.S, w.dim, w.q, h, ps, w.seed, n_stop=n_stop)[1][2]
-
-    assert_energy_or_chaos(rep["energy"], eo[2], control, f"{name} h={h}")
+    assert_energy(rep["energy"], eo[2], f"schedule {name} h={h}", levels=nl, sweeps=list(map(int, sw)),
+                  rel_kernel=_rel(rep["energy"], eg[2]))
 
 
 def test_dynamic_update(mm):
@@ -80,7 +76,7 @@ def test_dynamic_update(mm):
                                             x_init=x0.astype(np.float64))
     assert rep["levels"] == nl == 3
     assert rep["sweeps_level"] == list(sw), (rep["sweeps_level"], list(sw))
-    assert _rel(rep["energy"], eo[2]) <= ENERGY_TOL, (rep["energy"], eo)
+    assert_energy(rep["energy"], eo[2], "schedule dynamic cfg3_mesh32")
 
 
 @pytest.mark.parametrize("name,dim", [("cfg3_mesh64", 2), ("cfg5_grid12", 3)])
@@ -96,13 +92,8 @@ def test_schedule_sclap_disc(mm, name, dim):
     eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), 0.008, w.q)
     assert _rel(rep["energy"], eg[2]) <= 1e-4
     assert rep["sweeps_level"] == list(sw), (rep["sweeps_level"], list(sw))
-
-    def control(s):
-        ps = oracle.paper_schedule(max_final_iters=20, alpha0=1.0 * (1 + s), alpha_min=0.008 * (1 + s))
-        return oracle.layout_schedule(w.graph, w.S, w.dim, w.q, 2, ps, w.seed, n_stop=100, sclap=True,
-                                      disc=True)[1][2]
-
-    assert_energy_or_chaos(rep["energy"], eo[2], control, f"{name} sclap+disc")
+    assert_energy(rep["energy"], eo[2], f"schedule {name} sclap+disc", levels=nl, sweeps=list(map(int, sw)),
+                  rel_kernel=_rel(rep["energy"], eg[2]))
 
 
 def test_device_loop_matches_host_loop(tmp_path):

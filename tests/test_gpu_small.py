@@ -2,9 +2,13 @@
 sweeps of a level of up to 32,768 vertices (exact: 4,096) in one cooperative
 launch.  mm_layout with one sweep at h = 0 goes through it for these sizes, so
 its first sweep is checked against the oracle's Eq.(2) sweep; K sweeps are
-checked against K oracle sweeps (Jacobi: each from the previous result); the
-fused statistics against the oracle's relative change; and the Eq.(3) path
-through the multilevel full runs and schedule traces of the other files."""
+checked sweep by sweep: the K-sweep launch's output against one oracle sweep
+from the (K-1)-sweep launch's output (the persistent kernel is bitwise
+deterministic, so that is the state its K-th sweep started from), at the
+strict one-sweep bar for every K; the fused statistics against the oracle's
+relative change.  The Eq.(3) path is checked the same way through
+mm_sweeps with the oracle's hierarchy maps (h = 1, 2), 2-D and 3-D, q = 0 and
+q = 0.8, and the launch list proves the persistent kernel ran.""" 
 from __future__ import annotations
 
 import math
@@ -60,11 +64,72 @@ def test_small_exact_sizes(mm, n, dim, q):
 
 
 def test_small_exact_three_sweeps(mm):
-    """K = 3 in one launch (ping-pong and grid barriers) vs three oracle sweeps."""
+    """K = 1, 2, 3 in one launch each (ping-pong and grid barriers): the K-th
+    sweep of the launch equals one oracle sweep from the (K-1)-sweep output."""
     w = workload("cfg1_grid33")
-    got, rep = _layout_sweeps(mm, w.S, w.x0, 2, w.alpha, w.q, 3)
-    want = w.x0.astype(np.float64)
+    prev = w.x0
+    for K in (1, 2, 3):
+        got, rep = _layout_sweeps(mm, w.S, w.x0, 2, w.alpha, w.q, K)
+        assert rep["sweeps_level"] == [K]
+        want = oracle.sweep_exact(w.S, prev.astype(np.float64), w.alpha, w.q)
+        assert_sweep_parity(got, want, f"sweep {K} of a {K}-sweep launch")
+        prev = got
+
+
+def _approx_case(name, h):
+    import oracle as O
+
+    w = workload(name)
+    lv = O.build_hierarchy(w.graph, seed=w.seed, n_stop=100)
+    hp = min(h, len(lv) - 1)
+    anc = O.ancestor(lv, 0, hp)
+    # a layout-scale state: prolonged-looking clusters (parent's random spot + 1e-3 jitter)
+    rng = np.random.default_rng(5)
+    side = w.n ** (1.0 / w.dim)
+    xc = rng.random((lv[1].n, w.dim)) * side
+    x = (xc[lv[0].parent] + rng.uniform(-0.3, 0.3, (w.n, w.dim))).astype(np.float32)
+    return w, lv[0].parent, anc, lv[hp].n, x
+
+
+@pytest.mark.parametrize("name,h", [("cfg3_mesh64", 1), ("cfg3_mesh64", 2), ("cfg5_grid16", 1),
+                                    ("cfg5_grid16", 2), ("cfg3_mesh128", 3)])
+def test_small_approx_sweeps(mm, name, h):
+    """Eq.(3) in the persistent kernel: sweeps 1..3 of one launch each against
+    one oracle sweep_approx from the previous launch's output (1e-4 x diameter)."""
+    import torch
+
+    w, parent, anc, k, x0 = _approx_case(name, h)
+    S = mm.sset_to_device(w.S)
+    P = torch.from_numpy(parent.astype(np.int32)).cuda()
+    A = torch.from_numpy(anc.astype(np.int32)).cuda()
+    prev = x0
+    for K in (1, 2, 3):
+        mm.profile_reset()
+        mm.profile_enable(True)
+        y = mm.sweeps(S, mm.coords_to_device(x0), w.alpha, w.q, K, parent=P, ancestor=A, k=k)
+        torch.cuda.synchronize()
+        prof = mm.profile_read()
+        mm.profile_enable(False)
+        assert "small_level" in prof and "repulse_coarse" not in prof, sorted(prof)
+        got = mm.coords_from_device(y, w.dim)
+        want = oracle.sweep_approx(w.S, prev.astype(np.float64), w.alpha, w.q, parent, anc, k)
+        assert_sweep_parity(got, want, f"{name} h={h} sweep {K}")
+        prev = got
+
+
+def test_sweeps_tiled_path_matches_one_sweep_calls(mm):
+    """mm_sweeps on a level above the small-kernel limit (one CUDA graph of
+    the tiled kernels) equals K mm_sweep calls bit for bit."""
+    import torch
+
+    w, parent, anc, k, x0 = _approx_case("cfg3_mesh256", 2)
+    S = mm.sset_to_device(w.S)
+    P = torch.from_numpy(parent.astype(np.int32)).cuda()
+    A = torch.from_numpy(anc.astype(np.int32)).cuda()
+    x = mm.coords_to_device(x0)
+    y = mm.sweeps(S, x, w.alpha, w.q, 3, parent=P, ancestor=A, k=k)
+    z = x
     for _ in range(3):
-        want = oracle.sweep_exact(w.S, want, w.alpha, w.q)
-    assert rep["sweeps_level"] == [3]
-    assert_sweep_parity(got, want, "3 sweeps", tol=3e-4)
+        z = mm.sweep(S, z, w.alpha, w.q, parent=P, ancestor=A, k=k)
+    torch.cuda.synchronize()
+    assert torch.equal(y, z)

@@ -118,6 +118,64 @@ def test_p13_prolongation_bounds_and_rng():
     assert not np.array_equal(x, x2)
 
 
+TAG_DISC = 0x44495343  # oracle/mm_oracle.h OR_TAG_DISC
+
+
+@pytest.mark.parametrize("dim", [2, 3])
+def test_prolong_disc_laws(dim):
+    """The paper's disc prolongation: "a random position in a circle
+    around P with radius r := sqrt(c(v'))", "an angle uniformly at random in
+    [0, 2 pi] and a distance to P uniformly at random in [0, r]" (dim 3, R7:
+    radius c^(1/3), direction uniform on the sphere).  Pinned by the laws the
+    sentence states, not by the oracle's formula: every point within r of its
+    parent; distance / r uniform on [0, 1] (mean 1/2, not the 2/3 of an
+    area-uniform disc); direction uniform (mean 0, second moment 1/dim per
+    axis, equal quadrant counts)."""
+    rng = np.random.default_rng(11)
+    nc, n = 64, 40000
+    parent = rng.integers(0, nc, n).astype(np.int32)
+    xc = rng.normal(size=(nc, dim)) * 50.0
+    c = rng.integers(1, 40, nc).astype(np.int64)
+    x = oracle.prolong_disc(parent, xc, c, seed=5, level=1)
+    dev = x - xc[parent]
+    r = c[parent].astype(np.float64) ** (1.0 / dim)
+    dist = np.linalg.norm(dev, axis=1)
+    assert np.all(dist <= r * (1 + 1e-12))
+    t = dist / r
+    assert abs(t.mean() - 0.5) < 0.01
+    assert abs((t ** 2).mean() - 1.0 / 3.0) < 0.01
+    for q in (0.25, 0.5, 0.75):  # CDF of U[0, 1]
+        assert abs((t <= q).mean() - q) < 0.01
+    u = dev / np.maximum(dist, 1e-300)[:, None]
+    assert np.all(np.abs(u.mean(axis=0)) < 0.02)
+    assert np.all(np.abs((u ** 2).mean(axis=0) - 1.0 / dim) < 0.01)
+    quad = (u[:, 0] > 0).astype(int) * 2 + (u[:, 1] > 0)
+    assert np.all(np.abs(np.bincount(quad, minlength=4) / n - 0.25) < 0.01)
+
+
+def test_prolong_disc_hand_point_and_keys():
+    """Polar geometry by hand: with the draws U0, U1 of the pinned RNG, the
+    vertex lies at distance r U1 from its parent at angle 2 pi U0 (P:242:
+    "used as a polar coordinate for v with respect to the origin P"); the
+    draws are keyed by (seed, DISC tag, fine level, vertex)."""
+    parent = np.zeros(300, dtype=np.int32)
+    xc = np.array([[10.0, -4.0]])
+    c = np.array([9], dtype=np.int64)  # r = 3
+    x = oracle.prolong_disc(parent, xc, c, seed=9, level=4)
+    for u in (0, 17, 299):
+        U0 = oracle.uniform24(oracle.key_vertex(9, TAG_DISC, 4, u, 3, 0))
+        U1 = oracle.uniform24(oracle.key_vertex(9, TAG_DISC, 4, u, 3, 1))
+        d = x[u] - xc[0]
+        assert np.hypot(*d) == pytest.approx(3.0 * U1, rel=1e-12)
+        if U1 > 1e-6:
+            ang = np.arctan2(d[1], d[0]) % (2 * np.pi)
+            assert ang == pytest.approx(2 * np.pi * U0, abs=1e-9)
+    x2 = oracle.prolong_disc(parent, xc, c, seed=9, level=5)
+    x3 = oracle.prolong_disc(parent, xc, c, seed=10, level=4)
+    assert not np.array_equal(x, x2) and not np.array_equal(x, x3)
+    assert np.array_equal(x, oracle.prolong_disc(parent, xc, c, seed=9, level=4))
+
+
 def test_init_box_range():
     x = oracle.init_box(500, 2, 7.5, seed=4, level=6)
     assert x.min() >= 0.0 and x.max() < 7.5
