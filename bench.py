@@ -2,12 +2,17 @@
 """MulMent hot-path benchmark (driver contract).
 
 A STEP is one pass of the whole hot path over one batch of synthetic input:
-one mm_layout call on BASELINE.json configs[1] (RGG, n = 65,428 after LCC,
-S = hop <= 2 pairs, q = 0, alpha = 0.01, 20 exact Jacobi sweeps + the final
-Eq.(1) energy).  `value` = vertex-updates/s (n x sweeps per step, summed over
-ranks) with inputs resident in HBM; `e2e` = the same metric through the public
-API with the inputs copied from pinned host memory and the layout + energy
-copied back inside the timed region.
+one mm_layout call.  Default workload: BASELINE.json configs[4] (cfg5), the
+largest single-GPU config: 128^3 grid graph (n = 2,097,152), dim 3, q = 0.8,
+alpha = 0.01, hierarchy by heavy-edge matching, h = 2 coarse-representative
+repulsion (Eq.(3)), 15 sweeps per level, then the final Eq.(1) energy.  The
+step contains every §8(a) row: hierarchy build (matching, contraction, coarse
+S), box init, prolongation, centroid refresh, kernels (c)/(b)/(a), fused
+statistics, energy.  `value` = vertex-updates/s (sum over levels of n_l x
+sweeps, summed over ranks) with inputs resident in HBM; `e2e` = the same
+metric through the public API with the inputs copied from pinned host memory
+and the layout + energy copied back inside the timed region.  --config cfg1..4
+selects the other configs (parity-test cases / builder lines under profiles/).
 
 Multi-GPU: the north star is one GPU with no sharding, so --gpus N runs N
 independent replicas ("replicas only"); value = units of all
@@ -15,7 +20,7 @@ ranks / max-over-ranks time.
 
 --impl reference: this build has no installable reference implementation; the
 reference arm is the FP64 oracle (oracle/), timed as it stands on the host
-cores on a bounded row sample of the same sweep.
+cores on a bounded row sample of the same workload's sweep.
 """
 from __future__ import annotations
 
@@ -37,8 +42,19 @@ UNIT = "vertex-updates/s"
 SM_COUNT, FP32_LANES, SM_MAX_MHZ = 148, 128, 1965.0
 FP32_PEAK_TFLOPS = SM_COUNT * FP32_LANES * 2 * SM_MAX_MHZ * 1e6 / 1e12  # 74.4, derived
 MUFU_PER_CLK_SM = 16
-FLOP_PER_PAIR = 10  # 2D q = 0 pair: 2 sub + 2 fma (r^2) + 2 fma (acc), FMA = 2
-FLOP_PER_PAIR_COARSE = 11  # + the nu(v') weight
+
+
+def flop_per_pair(dim: int, q: float, coarse: bool) -> int:
+    """Algorithmic FP32 flop per pair interaction, SURVEY §8(d) (FMA = 2):
+    dim subtractions + dim FMA (r^2) + dim FMA (accumulation) + 1 FMUL of the
+    exponent (q > 0: 2^((q+2)/2 * -lg2 r^2)) + 1 FMUL of nu (coarse).
+    2-D q = 0 exact: 10; 2-D q = 0 coarse: 11; 3-D q = 0.8 coarse (cfg5): 17."""
+    return 5 * dim + (1 if q != 0.0 else 0) + (1 if coarse else 0)
+
+
+def mufu_per_pair(q: float) -> int:
+    """MUFU (XU) ops per pair: rcp (q = 0) or lg2 + ex2 (q > 0), SURVEY §8(d)."""
+    return 2 if q != 0.0 else 1
 
 
 # ------------------------------------------------------------------ distributed plumbing
@@ -241,7 +257,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": dict(config_block(w, args), l2="n/a: CPU oracle, host wall clock per step"),
+            "data": "synthetic", "config": config_block(w, args),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "pair_interactions_per_s": value * (w.n - 1) if w.h == 0 else None}
@@ -371,15 +387,17 @@ def run_gpu(args):
 
         e2e_step()
         torch.cuda.synchronize(dev)
-        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        # long steps (cfg5: seconds each): a few e2e steps bound the run time
+        e2e_steps = args.steps if ms_step < 1000.0 else min(args.steps, 3)
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
         barrier()
-        for s in range(args.steps):
+        for s in range(e2e_steps):
             flush.fill_(float(s))
             ev2[s][0].record(stream)
             e2e_step()
             ev2[s][1].record(stream)
         torch.cuda.synchronize(dev)
-        e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev2) / args.steps, dev)
+        e2e_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in ev2) / e2e_steps, dev)
 
     units = sum_over_ranks(float(rep["vertex_updates"]), dev)
     value = units / (ms_step / 1e3)
@@ -403,9 +421,8 @@ def run_gpu(args):
     else:
         nL = rep["n_level"][-1]
         pairs_launch = (pairs_step - nL * (nL - 1) * K) / max(kern["launches"] / prof_steps, 1)
-    flop_pair = FLOP_PER_PAIR if hh == 0 else FLOP_PER_PAIR_COARSE
-    if w.q != 0.0:
-        flop_pair += 3
+    flop_pair = flop_per_pair(w.dim, w.q, hh != 0)
+    mufu_pair = mufu_per_pair(w.q)
     achieved_tflops = flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
     # kernel (b) variant: the symmetric kernel evaluates every unordered pair
     # once, so it EXECUTES (flop_pair + 2 dim)/2 flop per ordered
@@ -414,6 +431,17 @@ def run_gpu(args):
     sym = hh == 0 and not small and mm.exact_kernel_variant(n, w.dim) == 1
     exec_flop_pair = (flop_pair + 2 * w.dim) / 2.0 if sym else float(flop_pair)
     executed_tflops = exec_flop_pair * pairs_launch / (k_ms / 1e3) / 1e12
+    pairs_s_kernel = pairs_launch / (k_ms / 1e3)
+    # MUFU ceiling: 16 XU ops/clk/SM at the max SM clock; the symmetric kernel
+    # executes one MUFU per UNORDERED pair, i.e. half per ordered pair
+    exec_mufu_pair = mufu_pair / 2.0 if sym else float(mufu_pair)
+    mufu_ceiling = SM_COUNT * MUFU_PER_CLK_SM * SM_MAX_MHZ * 1e6 / exec_mufu_pair
+    fp32_meas = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp32_peak.json")) as f:
+            fp32_meas = json.load(f)
+    except (OSError, ValueError):
+        fp32_meas = None
     step_share = {k: v["total_ms"] / max(prof_steps * dev_ms / args.steps, 1e-9) for k, v in prof.items()}
     gpu_ms = sum(v["total_ms"] for v in prof.values())
     gpu_share = {k: v["total_ms"] / max(gpu_ms, 1e-9) for k, v in prof.items()}
@@ -470,17 +498,22 @@ def run_gpu(args):
                      "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved_tflops / FP32_PEAK_TFLOPS,
                      "traffic": traffic, "traffic_unit": "bytes/launch (ncu dram read+write)",
                      "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x 1965 MHz (DESIGN.md §5)",
-                     "flop_per_pair": flop_pair, "pairs_per_launch": pairs_launch,
-                     "avg_launch_ms": k_ms,
+                     "flop_per_pair": flop_pair, "flop_per_pair_source": "SURVEY §8(d): 5 dim + (q>0) + coarse",
+                     "pairs_per_launch": pairs_launch, "avg_launch_ms": k_ms,
                      "kernel_variant": ("persistent small-level (all sweeps in one launch; latency-bound: "
                                         "grid barriers per sweep)") if small else ("symmetric" if sym else "one-sided"),
+                     # FP32 pipe utilisation: the flops the kernel EXECUTES (the symmetric kernel
+                     # evaluates each unordered pair once) over the same peak
                      "executed_flop_per_pair": exec_flop_pair,
                      "executed_tflops": executed_tflops, "executed_frac": executed_tflops / FP32_PEAK_TFLOPS,
-                     # the frac a kernel reaches at 16 MUFU ops/clk/SM with one MUFU per pair (q = 0)
-                     # or two (q > 0: lg2 + ex2), before batching / polynomial 2^y (Q29)
-                     "mufu_ceiling_frac": None if sym else
-                     MUFU_PER_CLK_SM / (2.0 if w.q != 0.0 else 1.0) * flop_pair / (2.0 * FP32_LANES),
-                     "pairs_per_s_kernel": pairs_launch / (k_ms / 1e3)},
+                     "executed_frac_of_measured_ffma_peak": (executed_tflops / fp32_meas["tflops"]
+                                                             if fp32_meas else None),
+                     "measured_ffma_peak": fp32_meas,
+                     "pairs_per_s_kernel": pairs_s_kernel,
+                     # the XU (MUFU) ceiling: SURVEY §8(d) counts 1 MUFU per pair at q = 0 (rcp) and 2 at
+                     # q > 0 (lg2 + ex2); kernel (c) moves part of the ex2 to the FMA pipe (Q29)
+                     "mufu_per_pair": mufu_pair, "mufu_ceiling_pairs_per_s": mufu_ceiling,
+                     "mufu_ceiling_frac": pairs_s_kernel / mufu_ceiling},
         "levels": rep["n_level"], "k_levels": rep["k_level"],
         # what the timed step computed (last step's report): Eq.(1) of the final layout (coincident
         # non-S pairs, possible in FP32, are left out and counted: DESIGN.md Q6) and the last sweep's
@@ -491,7 +524,7 @@ def run_gpu(args):
         "kernel_share_of_gpu_time": gpu_share,
         "kernels": prof,
         "cpu_baseline": cpu,
-        "e2e": {"value": units / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms,
+        "e2e": {"value": units / (e2e_ms / 1e3), "unit": UNIT, "ms_per_step": e2e_ms, "steps": e2e_steps,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
         "gpu_launches": launches,
         "clocks": clk,
@@ -507,7 +540,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="mm", choices=["mm", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--cpu-s", type=float, default=10.0)
     ap.add_argument("--ref-step-s", type=float, default=6.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")

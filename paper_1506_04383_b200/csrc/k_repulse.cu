@@ -94,6 +94,48 @@ __device__ __forceinline__ f2x ex2_poly2(f2x y) {
     return pk(__int_as_float(__float_as_int(p0) + (n0 << 23)), __int_as_float(__float_as_int(p1) + (n1 << 23)));
 }
 
+// 2^(c L) for a packed pair of L = lg2 r^2 on the FMA and ALU pipes, with the
+// scale c folded into the range reduction (no separate multiply): L is clamped
+// to [lmin, lmax] = [126/c, -125/c] (c < 0) so that c L stays in [-125, 126];
+// t = c L + 1.5 2^23 rounds c L to the nearest integer n, f = c L - n by one
+// FMA (exact product), then the degree-5 fit of ex2_poly2.
+// CLAMP = false: the caller guarantees c L <= 126 (r^2 >= kEps2 and
+// q <= kQNoClamp), so only the lower bound is applied.
+template <bool CLAMP>
+__device__ __forceinline__ f2x ex2_poly2_scaled(f2x L, float c, float lmin, float lmax) {
+    constexpr float kShift = 12582912.0f;
+    float l0, l1;
+    upk(L, l0, l1);
+    if constexpr (CLAMP) {
+        l0 = fmaxf(l0, lmin);
+        l1 = fmaxf(l1, lmin);
+    }
+    l0 = fminf(l0, lmax);
+    l1 = fminf(l1, lmax);
+    const f2x lc = pk(l0, l1);
+    const f2x cc = pk(c, c);
+    const f2x t = fma2(lc, cc, pk(kShift, kShift));
+    float t0, t1;
+    upk(t, t0, t1);
+    const f2x nn = fma2(t, pk(-1.f, -1.f), pk(kShift, kShift));  // -n, exact
+    const f2x f = fma2(lc, cc, nn);                               // c L - n
+    f2x p = pk(0.0013266970636323094f, 0.0013266970636323094f);
+    p = fma2(p, f, pk(0.009675459936261177f, 0.009675459936261177f));
+    p = fma2(p, f, pk(0.05550742521882057f, 0.05550742521882057f));
+    p = fma2(p, f, pk(0.24022121727466583f, 0.24022121727466583f));
+    p = fma2(p, f, pk(0.6931469440460205f, 0.6931469440460205f));
+    p = fma2(p, f, pk(1.0000001192092896f, 1.0000001192092896f));
+    float p0, p1;
+    upk(p, p0, p1);
+    // (t_bits - 0x4B400000) << 23 == t_bits << 23 (mod 2^32): one LEA per value
+    return pk(__int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23)),
+              __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23)));
+}
+
+#ifndef MM_POLY_FUSED
+#define MM_POLY_FUSED 1
+#endif
+
 #ifndef MM_POLY_MASK3
 #define MM_POLY_MASK3 0x11  // 3-D q > 0: sources 0 and 4 of every 8 take the polynomial 2^y (Q29; measured best of 0x11, 0x25, 0x49, 0x55)
 #endif
@@ -107,7 +149,7 @@ __device__ __forceinline__ f2x ex2_poly2(f2x y) {
 // sum.  LO: difference against the representative as (x_i - hi) - lo (Q24);
 // without it (x_i - hi) only, for tiles far from every target of the warp
 // (Q27).  POLY (q > 0): 2^y by ex2_poly2 instead of MUFU.EX2 (Q29).
-template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, bool PAIR_NU, bool LO, bool POLY>
+template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, bool PAIR_NU, bool LO, bool POLY, bool CLAMP>
 __device__ __forceinline__ void source_pairs(int jj, const float4* sm_a, const float4* sm_b, const f2x (&X)[G],
                                              const f2x (&Y)[G], const f2x (&Z)[G], f2x (&TX)[G], f2x (&TY)[G],
                                              f2x (&TZ)[G], float cexp) {
@@ -151,7 +193,18 @@ __device__ __forceinline__ void source_pairs(int jj, const float4* sm_a, const f
         if constexpr (QPOW && POLY) {
             float r0, r1;
             upk(r2, r0, r1);
-            inv = ex2_poly2(mul_bc(pk(lg2_approx(r0), lg2_approx(r1)), cexp));
+            if constexpr (MM_POLY_FUSED != 0)
+                inv = ex2_poly2_scaled<CLAMP>(pk(lg2_approx(r0), lg2_approx(r1)), cexp, kExpClamp / cexp,
+                                              -125.f / cexp);
+            else
+                inv = ex2_poly2(mul_bc(pk(lg2_approx(r0), lg2_approx(r1)), cexp));
+            if constexpr (PAIR_NU) inv = mul_bc(inv, nu);
+        } else if constexpr (QPOW && !CLAMP) {
+            // 2^(c lg2 r^2) with c lg2 r^2 <= 126 guaranteed (no clamp); packed scale
+            float r0, r1, y0, y1;
+            upk(r2, r0, r1);
+            upk(mul_bc(pk(lg2_approx(r0), lg2_approx(r1)), cexp), y0, y1);
+            inv = pk(ex2_approx(y0), ex2_approx(y1));
             if constexpr (PAIR_NU) inv = mul_bc(inv, nu);
         } else if constexpr (PAIR_NU) {
             // all k representatives, the own one H(i) included: kernel (a)
@@ -175,7 +228,7 @@ __device__ __forceinline__ void source_pairs(int jj, const float4* sm_a, const f
 }
 
 // One shared-memory source tile (cnt sources) against the thread's targets.
-template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, int UNR, bool PAIR_NU, bool LO>
+template <int DIM, bool QPOW, bool COARSE, int G, int BMASK, int UNR, bool PAIR_NU, bool LO, bool CLAMP>
 __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const float4* sm_b, const f2x (&X)[G],
                                            const f2x (&Y)[G], const f2x (&Z)[G], f2x (&TX)[G], f2x (&TY)[G],
                                            f2x (&TZ)[G], float cexp) {
@@ -184,7 +237,7 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
     if constexpr (PM != 0) {
         // blocks of 8 sources with a fixed MUFU / polynomial split (Q29)
 #define MM_SRC(u) \
-    source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, ((PM >> (u)) & 1) != 0>(jj + (u), sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp)
+    source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, ((PM >> (u)) & 1) != 0, CLAMP>(jj + (u), sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp)
         for (; jj + 8 <= cnt; jj += 8) {
             MM_SRC(0); MM_SRC(1); MM_SRC(2); MM_SRC(3); MM_SRC(4); MM_SRC(5); MM_SRC(6); MM_SRC(7);
         }
@@ -192,10 +245,10 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
     }
 #pragma unroll UNR
     for (; jj < cnt; ++jj)
-        source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, false>(jj, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp);
+        source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, false, CLAMP>(jj, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp);
 }
 
-template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4>
+template <int DIM, bool QPOW, bool COARSE, int T, int BMASK = 1, int MINB = 1, int UNR = 4, bool CLAMP = true>
 __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const float* __restrict__ x, int32_t n_src,
                                                     const float4* __restrict__ rep_hi,
                                                     const float4* __restrict__ rep_lo, CoarseOrder co, float cexp,
@@ -306,10 +359,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
             }
             if (tnu > 0) {
                 if (far)
-                    tile_pairs<DIM, QPOW, COARSE, G, kFastMask, UNR, false, false>(cnt, sm_a, sm_b, X, Y, Z, TX, TY,
+                    tile_pairs<DIM, QPOW, COARSE, G, kFastMask, UNR, false, false, CLAMP>(cnt, sm_a, sm_b, X, Y, Z, TX, TY,
                                                                                  TZ, cexp);
                 else
-                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, false, COARSE>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
+                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, false, COARSE, CLAMP>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
                                                                                cexp);
                 const f2x nu2 = pk((float)tnu, (float)tnu);
 #pragma unroll
@@ -320,10 +373,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_repulse(int32_t n_tgt, const f
                 }
             } else {
                 if (far)
-                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE, false>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
+                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE, false, CLAMP>(cnt, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
                                                                                cexp);
                 else
-                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE, COARSE>(cnt, sm_a, sm_b, X, Y, Z, TX, TY,
+                    tile_pairs<DIM, QPOW, COARSE, G, BMASK, UNR, COARSE, COARSE, CLAMP>(cnt, sm_a, sm_b, X, Y, Z, TX, TY,
                                                                                 TZ, cexp);
 #pragma unroll
                 for (int gg = 0; gg < G; ++gg) {
@@ -838,11 +891,15 @@ constexpr int kBatchMask = (DIM == 2 && !QPOW) ? (COARSE ? MM_COARSE_BMASK : 1) 
 template <int DIM, bool QPOW, bool COARSE>
 constexpr int kMinB = (DIM == 3 && QPOW && COARSE) ? MM_C3_MINB : (DIM == 2 && COARSE) ? MM_C2_MINB : 1;
 
-template <int DIM, bool QPOW, bool COARSE, int T>
+// q > 0 with (q + 2)/2 * |lg2 kEps2| <= 126: 2^(c lg2 r^2) cannot overflow, the
+// kernels skip the upper clamp (CLAMP = false)
+constexpr float kQNoClamp = 2.2f;
+
+template <int DIM, bool QPOW, bool COARSE, int T, bool CLAMP = true>
 int resident_ctas() {
     static const int occ = [] {  // per instantiation; queried once
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>, kMinB<DIM, QPOW, COARSE>, MM_REP_UNR>,
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_repulse<DIM, QPOW, COARSE, T, kBatchMask<DIM, QPOW, COARSE>, kMinB<DIM, QPOW, COARSE>, MM_REP_UNR, CLAMP>,
                                                       kBlock, 0);
         return o > 0 ? o : 1;
     }();
@@ -902,9 +959,11 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
     LaunchScope ls(coarse ? "repulse_coarse" : "repulse_exact", st);
 // batched reciprocals (BMASK) in half of the target groups for 2-D q = 0
 // (exact and coarse: measured faster by tools/ubench_repulse.cu); none for q > 0.
-#define MM_LAUNCH(D, Q, C, T) \
-    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>, kMinB<D, Q, C>, MM_REP_UNR><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, co, cexp,  \
+#define MM_LAUNCH_CL(D, Q, C, T, CL) \
+    k_repulse<D, Q, C, T, kBatchMask<D, Q, C>, kMinB<D, Q, C>, MM_REP_UNR, CL><<<p.sch.G, kBlock, 0, st>>>(n_tgt, x, n_src, rep_hi, rep_lo, co, cexp,  \
                                                                           p.sch, part)
+#define MM_LAUNCH(D, Q, C, T) \
+    do { if (Q && q <= kQNoClamp) MM_LAUNCH_CL(D, Q, C, T, false); else MM_LAUNCH_CL(D, Q, C, T, true); } while (0)
     if (dim == 2) {
         if (!qpow && !coarse) MM_LAUNCH(2, false, false, MM_T2);
         else if (!qpow && coarse) MM_LAUNCH(2, false, true, MM_T2);
@@ -917,6 +976,7 @@ cudaError_t launch_repulse(int dim, bool qpow, bool coarse, float q, int32_t n_t
         else MM_LAUNCH(3, true, true, MM_T3);
     }
 #undef MM_LAUNCH
+#undef MM_LAUNCH_CL
     return cudaGetLastError();
 }
 

@@ -117,19 +117,51 @@ def test_small_approx_sweeps(mm, name, h):
         prev = got
 
 
-def test_sweeps_tiled_path_matches_one_sweep_calls(mm):
-    """mm_sweeps on a level above the small-kernel limit (one CUDA graph of
-    the tiled kernels) equals K mm_sweep calls bit for bit."""
+@pytest.mark.parametrize("approx", [False, True])
+def test_small_coincident_points(mm, approx):
+    """The persistent kernel with exactly coincident S and non-S pairs (Q6)."""
+    import torch
+
+    from tests.test_gpu_sweep import _coincident_state
+
+    w = workload("cfg3_mesh64")
+    x0 = _coincident_state(w.S, w.n, 2, seed=41)
+    S = mm.sset_to_device(w.S)
+    if approx:
+        lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=100)
+        anc = oracle.ancestor(lv, 0, 2)
+        k = lv[2].n
+        y = mm.sweeps(S, mm.coords_to_device(x0), w.alpha, w.q, 1, parent=torch.from_numpy(lv[0].parent).cuda(),
+                      ancestor=torch.from_numpy(anc.astype(np.int32)).cuda(), k=k)
+        want = oracle.sweep_approx(w.S, x0.astype(np.float64), w.alpha, w.q, lv[0].parent, anc, k)
+    else:
+        y = mm.sweeps(S, mm.coords_to_device(x0), w.alpha, w.q, 1)
+        want = oracle.sweep_exact(w.S, x0.astype(np.float64), w.alpha, w.q)
+    torch.cuda.synchronize()
+    assert_sweep_parity(mm.coords_from_device(y, 2), want, f"small coincident approx={approx}")
+
+
+def test_sweeps_tiled_path(mm):
+    """mm_sweeps on a level above the small-kernel limit (the K sweeps are one
+    CUDA graph of the tiled kernels, target / representative orders fixed per
+    call, Q26): sweep K of a K-sweep call against one oracle sweep from the
+    (K-1)-sweep call's output, at the strict bar."""
     import torch
 
     w, parent, anc, k, x0 = _approx_case("cfg3_mesh256", 2)
     S = mm.sset_to_device(w.S)
     P = torch.from_numpy(parent.astype(np.int32)).cuda()
     A = torch.from_numpy(anc.astype(np.int32)).cuda()
-    x = mm.coords_to_device(x0)
-    y = mm.sweeps(S, x, w.alpha, w.q, 3, parent=P, ancestor=A, k=k)
-    z = x
-    for _ in range(3):
-        z = mm.sweep(S, z, w.alpha, w.q, parent=P, ancestor=A, k=k)
-    torch.cuda.synchronize()
-    assert torch.equal(y, z)
+    prev = x0
+    for K in (1, 2, 3):
+        mm.profile_reset()
+        mm.profile_enable(True)
+        y = mm.sweeps(S, mm.coords_to_device(x0), w.alpha, w.q, K, parent=P, ancestor=A, k=k)
+        torch.cuda.synchronize()
+        prof = mm.profile_read()
+        mm.profile_enable(False)
+        assert "repulse_coarse" in prof and "small_level" not in prof, sorted(prof)
+        got = mm.coords_from_device(y, w.dim)
+        want = oracle.sweep_approx(w.S, prev.astype(np.float64), w.alpha, w.q, parent, anc, k)
+        assert_sweep_parity(got, want, f"tiled sweep {K}")
+        prev = got

@@ -144,6 +144,91 @@ def test_approx_sweep_full_size_sampled(mm, name, rows):
     assert_sweep_parity(got[r], want, f"{name} sampled")
 
 
+def _structured_state(name, lv, dim, disc: bool, offset: float):
+    """A clustered layout built only from the oracle's own steps: the level-2
+    clusters at a seeded box position (Q14's scale), prolonged to level 1 and
+    level 0 (Q15 jitter, or the paper's disc P:240-242), then shifted by
+    `offset` in every coordinate (cfg4's converged layouts sit at 885-1140,
+    where FP32 differences to a centroid cancel: Q24, Q28)."""
+    n2 = lv[2].n
+    x = oracle.init_box(n2, dim, float(lv[0].n) ** (1.0 / dim), seed=21, level=2)
+    for l in (1, 0):
+        if disc:
+            x = oracle.prolong_disc(lv[l].parent, x, lv[l + 1].c, seed=21, level=l)
+        else:
+            x = oracle.prolong(lv[l].parent, x, seed=21, level=l)
+    return (x + offset).astype(np.float32)
+
+
+@pytest.mark.parametrize("name,disc,rows", [("cfg4", True, 2048), ("cfg4", False, 1024), ("cfg5", True, 512)])
+def test_approx_sweep_full_size_structured(mm, name, disc, rows):
+    """Full-size Eq.(3) sweep from a clustered, offset state (not a random one):
+    representatives sit among their members, most tiles are near a warp's
+    targets, and the centroid differences need the hi/lo split (Q24-Q28)."""
+    w = workload(name)
+    lv = oracle_hierarchy(name)
+    anc = oracle.ancestor(lv, 0, 2)
+    k = lv[2].n
+    x = _structured_state(name, lv, w.dim, disc, 1000.0)
+    got = _gpu_sweep(mm, w.S, x, w.alpha, w.q, lv[0].parent, anc, k)
+    rl = w.S.row_lengths()
+    r = sample_rows(w.n, rows, seed=14, extra=np.argsort(rl)[-4:])
+    want = oracle.sweep_approx(w.S, x.astype(np.float64), w.alpha, w.q, lv[0].parent, anc, k, rows=r)
+    assert_sweep_parity(got[r], want, f"{name} structured disc={disc} sampled")
+
+
+def _coincident_state(S, n, dim, seed, count=25):
+    """A random state where `count` S pairs and `count` non-S pairs coincide
+    exactly (x_j := x_i bit for bit): Q6, both sides take such a pair's unit
+    vector and r-value as 0."""
+    rng = np.random.default_rng(seed)
+    x = configs.random_state(n, dim, seed=seed, scale=math.sqrt(n))
+    rp, col = S.row_ptr, S.col
+    used = set()
+    for i in rng.choice(n, count, replace=False):
+        j = int(col[rp[i] + rng.integers(0, rp[i + 1] - rp[i])])
+        if i in used or j in used:
+            continue
+        x[j] = x[i]
+        used.update((int(i), j))
+    placed = 0
+    while placed < count:
+        a, b = (int(v) for v in rng.choice(n, 2, replace=False))
+        if a in used or b in used or b in set(col[rp[a]:rp[a + 1]].tolist()):
+            continue
+        x[b] = x[a]
+        used.update((a, b))
+        placed += 1
+    return x
+
+
+@pytest.mark.parametrize("dim,q", [(2, 0.0), (3, 0.8), (2, 0.5), (3, 0.0)])
+def test_exact_sweep_coincident_points(mm, dim, q):
+    """Exactly coincident S pairs and non-S pairs (Q6): finite output equal to
+    the oracle's.  Run by every kernel (b) variant (test_gpu_sym.py forces
+    each)."""
+    n = 3001
+    g = H.random_connected(n, n // 2 + 1, seed=31)
+    S = sset.hop2_sset(g)
+    x = _coincident_state(S, n, dim, seed=32)
+    got = _gpu_sweep(mm, S, x, 0.05, q)
+    want = oracle.sweep_exact(S, x.astype(np.float64), 0.05, q)
+    assert_sweep_parity(got, want, f"coincident dim={dim} q={q}")
+
+
+@pytest.mark.parametrize("name,q", [("cfg3_mesh64", 0.0), ("cfg5_grid16", 0.8), ("cfg3_mesh128", 0.5)])
+def test_approx_sweep_coincident_points(mm, name, q):
+    """Kernel (c) + (a) with exactly coincident S pairs and non-S pairs (Q6)."""
+    w = workload(name)
+    lv = oracle_hierarchy(name)
+    anc = oracle.ancestor(lv, 0, 2)
+    k = lv[2].n
+    x = _coincident_state(w.S, w.n, w.dim, seed=33)
+    got = _gpu_sweep(mm, w.S, x, w.alpha, q, lv[0].parent, anc, k)
+    want = oracle.sweep_approx(w.S, x.astype(np.float64), w.alpha, q, lv[0].parent, anc, k)
+    assert_sweep_parity(got, want, f"{name} coincident q={q}")
+
+
 def test_approx_identity_map_equals_exact(mm):
     """P:281 on the GPU: M = identity makes Eq.(3) equal Eq.(2)."""
     w = workload("cfg2_rgg4096")
