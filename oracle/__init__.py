@@ -112,6 +112,9 @@ def lib() -> ctypes.CDLL:
     L.or_build_hierarchy_sclap.argtypes = [c_i32, _i64p, _i32p, _i64p, _i64p, c_u64, c_i32, c_i32, c_i32, c_dbl, c_dbl,
                                            ctypes.POINTER(ctypes.c_void_p)]
     L.or_sclap_labels.argtypes = [c_i32, _i64p, _i32p, _i64p, _i64p, c_i64, c_i32, c_u64, c_i32, _i32p]
+    L.or_sclap_labels_seq.argtypes = [c_i32, _i64p, _i32p, _i64p, _i64p, c_i64, c_i32, c_u64, c_i32, _i32p]
+    L.or_build_hierarchy_sclap_mode.argtypes = [c_i32, _i64p, _i32p, _i64p, _i64p, c_u64, c_i32, c_i32, c_i32, c_dbl,
+                                                c_dbl, c_int, ctypes.POINTER(ctypes.c_void_p)]
     _lib = L
     return L
 
@@ -237,9 +240,11 @@ class Level:
 
 def build_hierarchy(g, seed: int, n_stop: int = 1000, max_levels: int = 64, max_rounds: int = 64,
                     omega: Optional[np.ndarray] = None, c: Optional[np.ndarray] = None, sclap: bool = False,
-                    lp_rounds: int = 3, f0: float = 20.0, b: float = 2.0) -> List[Level]:
-    """Matching-based hierarchy (Q16/Q17) or SCLaP (sclap=True, P:202-223, R6);
-    contraction per P:225-232."""
+                    lp_rounds: int = 3, f0: float = 20.0, b: float = 2.0, sclap_seq: bool = False) -> List[Level]:
+    """Matching-based hierarchy (Q16/Q17) or SCLaP (sclap=True):
+    the synchronous reading R6 (the GPU's rule), or with sclap_seq=True the
+    paper's sequential random-order label propagation (R6s); contraction per
+    P:225-232."""
     rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
     col = np.ascontiguousarray(g.col, dtype=np.int32)
     om = None if omega is None else np.ascontiguousarray(omega, dtype=np.int64)
@@ -247,9 +252,10 @@ def build_hierarchy(g, seed: int, n_stop: int = 1000, max_levels: int = 64, max_
     h = ctypes.c_void_p()
     L = lib()
     if sclap:
-        _check(L.or_build_hierarchy_sclap(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
-                                          _p(om, ctypes.c_int64), _p(cc, ctypes.c_int64), seed, n_stop, max_levels,
-                                          lp_rounds, f0, b, ctypes.byref(h)), "build_hierarchy_sclap")
+        _check(L.or_build_hierarchy_sclap_mode(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
+                                               _p(om, ctypes.c_int64), _p(cc, ctypes.c_int64), seed, n_stop,
+                                               max_levels, lp_rounds, f0, b, 1 if sclap_seq else 0,
+                                               ctypes.byref(h)), "build_hierarchy_sclap")
     else:
         _check(L.or_build_hierarchy(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32),
                                     _p(om, ctypes.c_int64), _p(cc, ctypes.c_int64), seed, n_stop,
@@ -359,8 +365,10 @@ def layout(g, S, dim: int, alpha: float, q: float, h: int, sweeps, seed: int, n_
 
 def layout_schedule(g, S, dim: int, q: float, h: int, sched: Schedule, seed: int, n_stop: int = 1000,
                     multilevel: bool = True, dynamic: bool = False, x_init: Optional[np.ndarray] = None,
-                    nthreads: Optional[int] = None, sclap: bool = False, disc: bool = False):
-    """The paper's schedule or the dynamic update.
+                    nthreads: Optional[int] = None, sclap: bool = False, disc: bool = False,
+                    sclap_seq: bool = False):
+    """The paper's schedule (P:250-258) or the dynamic update (P:424-427);
+    sclap_seq: SCLaP by the paper's sequential label propagation (R6s).
     Returns (x0, (stress, entropy, total at alpha_min), levels, sweeps per level)."""
     rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
     col = np.ascontiguousarray(g.col, dtype=np.int32)
@@ -371,7 +379,8 @@ def layout_schedule(g, S, dim: int, q: float, h: int, sched: Schedule, seed: int
     en = np.zeros(3, dtype=np.float64)
     nl = ctypes.c_int32()
     sw = np.zeros(64, dtype=np.int32)
-    flags = (1 if multilevel else 0) | (2 if dynamic else 0) | (4 if sclap else 0) | (8 if disc else 0)
+    flags = ((1 if multilevel else 0) | (2 if dynamic else 0) | (4 if sclap else 0) | (8 if disc else 0)
+             | (16 if sclap_seq else 0))
     _check(lib().or_layout_schedule(n, dim, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(srp, ctypes.c_int64),
                                     _p(scol, ctypes.c_int32), _p(d, ctypes.c_double), _p(w, ctypes.c_double), q, h,
                                     ctypes.byref(sched), seed, n_stop, flags, _p(xi, ctypes.c_double),
@@ -393,14 +402,15 @@ def full_stress(g, x: np.ndarray, nthreads: Optional[int] = None):
     return float(out[0]), float(out[1]), float(out[2]), int(out[3])
 
 
-def sclap_labels(g, U: int, rounds: int, seed: int, level: int, omega=None, c=None) -> np.ndarray:
-    """One SCLaP clustering (R6) with size bound U; returns the labels."""
+def sclap_labels(g, U: int, rounds: int, seed: int, level: int, omega=None, c=None, seq: bool = False) -> np.ndarray:
+    """One SCLaP clustering with size bound U (R6, or seq=True: the paper's
+    sequential label propagation R6s); returns the labels."""
     rp = np.ascontiguousarray(g.row_ptr, dtype=np.int64)
     col = np.ascontiguousarray(g.col, dtype=np.int32)
     om = np.ascontiguousarray(np.ones(col.shape[0]) if omega is None else omega, dtype=np.int64)
     cc = np.ascontiguousarray(np.ones(g.n) if c is None else c, dtype=np.int64)
     lab = np.empty(g.n, dtype=np.int32)
-    _check(lib().or_sclap_labels(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(om, ctypes.c_int64),
-                                 _p(cc, ctypes.c_int64), U, rounds, seed, level, _p(lab, ctypes.c_int32)),
-           "sclap_labels")
+    fn = lib().or_sclap_labels_seq if seq else lib().or_sclap_labels
+    _check(fn(g.n, _p(rp, ctypes.c_int64), _p(col, ctypes.c_int32), _p(om, ctypes.c_int64),
+              _p(cc, ctypes.c_int64), U, rounds, seed, level, _p(lab, ctypes.c_int32)), "sclap_labels")
     return lab

@@ -238,6 +238,14 @@ int or_sclap_labels(int32_t n, const int64_t* rp, const int32_t* col, const int6
 int or_build_hierarchy_sclap(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega,
                              const int64_t* c, uint64_t seed, int32_t n_stop, int32_t max_levels, int32_t rounds,
                              double f0, double b, or_hierarchy** out) {
+    return or_build_hierarchy_sclap_mode(n, rp, col, omega, c, seed, n_stop, max_levels, rounds, f0, b, 0, out);
+}
+
+/* seq = 1: the paper's sequential label propagation (R6s, or_sclap_labels_seq);
+ * seq = 0: the synchronous reading R6 (or_sclap_labels) */
+int or_build_hierarchy_sclap_mode(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega,
+                                  const int64_t* c, uint64_t seed, int32_t n_stop, int32_t max_levels,
+                                  int32_t rounds, double f0, double b, int seq, or_hierarchy** out) {
     if (n <= 0 || !rp || !col || !out || max_levels < 1 || rounds < 1 || !(f0 > 0.0) || !(b > 1.0)) return OR_EINVAL;
     or_hierarchy* H = NULL;
     /* level 0 via the matching builder with max_levels = 1 (copies the graph) */
@@ -262,7 +270,8 @@ int or_build_hierarchy_sclap(int32_t n, const int64_t* rp, const int32_t* col, c
         if ((double)n / f < W) W = (double)n / f;
         const int64_t Wi = (int64_t)W; /* floor: cluster weights are integers */
         const int64_t U = cmax > Wi ? cmax : Wi;
-        rc = or_sclap_labels(g->n, g->rp, g->col, g->omega, g->c, U, rounds, seed, h - 1, lab);
+        rc = seq ? or_sclap_labels_seq(g->n, g->rp, g->col, g->omega, g->c, U, rounds, seed, h - 1, lab)
+                 : or_sclap_labels(g->n, g->rp, g->col, g->omega, g->c, U, rounds, seed, h - 1, lab);
         if (rc) break;
         g->rounds = rounds;
         or_level next;

@@ -75,6 +75,12 @@ int or_build_hierarchy(int32_t n, const int64_t* rp, const int32_t* col,
 int or_build_hierarchy_sclap(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega,
                              const int64_t* c, uint64_t seed, int32_t n_stop, int32_t max_levels, int32_t rounds,
                              double f0, double b, or_hierarchy** out);
+int or_build_hierarchy_sclap_mode(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega,
+                                  const int64_t* c, uint64_t seed, int32_t n_stop, int32_t max_levels,
+                                  int32_t rounds, double f0, double b, int seq, or_hierarchy** out);
+/* the paper's sequential label propagation (reading R6s in sclap.c) */
+int or_sclap_labels_seq(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega, const int64_t* c,
+                        int64_t U, int32_t rounds, uint64_t seed, int32_t level, int32_t* lab);
 int or_sclap_labels(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega, const int64_t* c,
                     int64_t U, int32_t rounds, uint64_t seed, int32_t level, int32_t* lab);
 int32_t or_hier_num_levels(const or_hierarchy* h);
@@ -117,7 +123,8 @@ int or_layout(int32_t n, int dim, const int64_t* rp, const int32_t* col,
  * at alpha_min on the finest level only, from x_init, with the hierarchy built
  * to at most h levels above the finest (the approximation level).
  * flags bit 2: SCLaP hierarchy (R6; lp_rounds = 3, f = 20, b = 2) instead of the
- * matching; bit 3: the paper's disc prolongation (R7) instead of Q15.
+ * matching; bit 3: the paper's disc prolongation (R7) instead of Q15;
+ * bit 4 (with bit 2): SCLaP by the paper's sequential label propagation (R6s). 
  * sweeps_out[l] = sweeps performed at level l (nullable, 64 entries). */
 typedef struct {
     double alpha0, alpha_min, factor, eps;

@@ -82,8 +82,8 @@ int or_layout_schedule(int32_t n, int dim, const int64_t* rp, const int32_t* col
         /* dynamic: stop the coarsening after h levels (the approximation level) */
         const int32_t max_levels = dynamic ? (h + 1) : 64;
         if (flags & 4)
-            rc = or_build_hierarchy_sclap(n, rp, col, NULL, NULL, seed, dynamic ? 1 : n_stop, max_levels, 3, 20.0, 2.0,
-                                          &H);
+            rc = or_build_hierarchy_sclap_mode(n, rp, col, NULL, NULL, seed, dynamic ? 1 : n_stop, max_levels, 3, 20.0,
+                                               2.0, (flags & 16) ? 1 : 0, &H);
         else
             rc = or_build_hierarchy(n, rp, col, NULL, NULL, seed, dynamic ? 1 : n_stop, max_levels, 64, &H);
         if (rc) { free(xa); free(xb); return rc; }

@@ -1,5 +1,11 @@
 /* ORACLE (test infrastructure only) — SCLaP coarsening,
- * integer-exact, in the synchronous reading R6 of DESIGN.md.
+ * integer-exact.  Two functions:
+ *   or_sclap_labels_seq  the paper's label propagation as written (reading
+ *                        R6s below): nodes visited one at a time in a random
+ *                        order, each move applied immediately;
+ *   or_sclap_labels      the synchronous reading R6 of DESIGN.md that the GPU
+ *                        implements (a parallel rule; checked against the
+ *                        sequential one for validity and quality in tests).
  *
  * label propagation "starts with a singleton clustering
  * ... in each round the algorithm visits all nodes ... and assigns each node to
@@ -49,6 +55,75 @@ typedef struct { int32_t L; int64_t w; } lw;
 static int cmp_lw(const void* a, const void* b) {
     const lw* x = (const lw*)a; const lw* y = (const lw*)b;
     return (x->L > y->L) - (x->L < y->L);
+}
+
+/* R6s, the paper's sequential label propagation: "starts with a
+ * singleton clustering", "works in rounds", "in each round the algorithm
+ * visits all nodes in random order and assigns each node to the predominant
+ * cluster in its neighborhood"; SCLaP: "nodes are assigned to the
+ * predominant cluster that is not overloaded after the label change", i.e.
+ * cw(L) + c(v) <= U for L != label(v).  Silences, read here: the random order
+ * of round r is a Fisher-Yates shuffle driven by the counter RNG of (seed,
+ * "LPSQ", level, r, i); "predominant" = largest sum of edge weights omega to
+ * the cluster; a node leaves its cluster only for a strictly larger score
+ * (ties with its own label keep it; ties among other labels: higher hash of
+ * (seed, level, r, v, L), then the lower label); labels and cluster weights
+ * are updated immediately, so later nodes of the round see the move.  Stop
+ * after `rounds` rounds (the paper's l) or a round without moves. */
+#define OR_TAG_LPSQ 0x4c505351ULL /* "LPSQ" */
+int or_sclap_labels_seq(int32_t n, const int64_t* rp, const int32_t* col, const int64_t* omega, const int64_t* c,
+                        int64_t U, int32_t rounds, uint64_t seed, int32_t level, int32_t* lab) {
+    int64_t* cw = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+    int64_t* acc = (int64_t*)calloc((size_t)(n > 0 ? n : 1), sizeof(int64_t));
+    int32_t* touched = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    int32_t* order = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+    if (!cw || !acc || !touched || !order) { free(cw); free(acc); free(touched); free(order); return OR_ENOMEM; }
+    for (int32_t v = 0; v < n; ++v) { lab[v] = v; cw[v] = c[v]; }
+    for (int32_t r = 0; r < rounds; ++r) {
+        /* random visiting order of this round */
+        const uint64_t k0 = or_mix64(or_mix64(or_mix64(seed ^ OR_TAG_LPSQ) ^ (uint64_t)level) ^ (uint64_t)r);
+        for (int32_t i = 0; i < n; ++i) order[i] = i;
+        for (int32_t i = n - 1; i > 0; --i) {
+            const int32_t j = (int32_t)(or_mix64(k0 ^ (uint64_t)i) % (uint64_t)(i + 1));
+            const int32_t t = order[i]; order[i] = order[j]; order[j] = t;
+        }
+        int32_t moved = 0;
+        for (int32_t t = 0; t < n; ++t) {
+            const int32_t v = order[t];
+            int32_t m = 0;
+            for (int64_t e = rp[v]; e < rp[v + 1]; ++e) {
+                const int32_t u = col[e];
+                if (u == v) continue;
+                const int32_t L = lab[u];
+                if (acc[L] == 0) touched[m++] = L;
+                acc[L] += omega[e];
+            }
+            const int32_t own = lab[v];
+            const int64_t s0 = acc[own];
+            int32_t best = -1;
+            int64_t bs = 0;
+            uint64_t bh = 0;
+            for (int32_t q = 0; q < m; ++q) {
+                const int32_t L = touched[q];
+                const int64_t s = acc[L];
+                if (L == own || cw[L] + c[v] > U) continue;
+                const uint64_t h = lp_hash(seed, level, r, v, L);
+                if (best < 0 || s > bs || (s == bs && (h > bh || (h == bh && L < best)))) {
+                    best = L; bs = s; bh = h;
+                }
+            }
+            for (int32_t q = 0; q < m; ++q) acc[touched[q]] = 0;
+            if (best >= 0 && bs > s0) {
+                cw[own] -= c[v];
+                cw[best] += c[v];
+                lab[v] = best;
+                ++moved;
+            }
+        }
+        if (moved == 0) break;
+    }
+    free(cw); free(acc); free(touched); free(order);
+    return 0;
 }
 
 /* One SCLaP clustering of graph (n, rp, col, omega, c) with bound U; labels out. */

@@ -70,9 +70,49 @@ def test_hierarchy_with_weights(mm):
         assert np.array_equal(H.level_host(l + 1)["omega"].astype(np.int64), want[l + 1].omega)
 
 
+@pytest.mark.parametrize("name", ["cfg3_mesh64", "cfg5_grid16", "cfg4_cl20000", "cfg3", "cfg5_grid64"])
+def test_sclap_hierarchy_valid(mm, name):
+    """The GPU's SCLaP hierarchy checked on its own, without the oracle, for
+    what the paper requires of a size-constrained clustering and its
+    contraction: every coarse node weighs at most
+    U <= max(max c, 2^h) (W = min(b^h, n/f), b = 2); node weights conserved;
+    parent maps onto every coarse id; the coarse graph is Pm^T A Pm without
+    self loops (edge weights = crossing sums); every contraction merges
+    something (a level that merges nothing is discarded, R6)."""
+    import scipy.sparse as sp
+
+    w = workload(name)
+    n_stop = 1000 if w.n > 50000 else 100
+    H = mm.build_hierarchy(mm.graph_to_device(w.graph), w.dim, w.seed, n_stop=n_stop, sclap=True)
+    assert H.num_levels >= 3
+    levels = [H.level_host(l) for l in range(H.num_levels)]
+    assert levels[0]["n"] == w.n
+    for l in range(H.num_levels - 1):
+        fine, coarse = levels[l], levels[l + 1]
+        n, k = int(fine["n"]), int(coarse["n"])
+        P = fine["parent"].astype(np.int64)
+        cf, cc = fine["c"].astype(np.int64), coarse["c"].astype(np.int64)
+        assert P.min() >= 0 and P.max() == k - 1 and np.unique(P).shape[0] == k
+        np.testing.assert_array_equal(np.bincount(P, weights=cf, minlength=k).astype(np.int64), cc)
+        assert cc.max() <= max(int(cf.max()), 2 ** (l + 1)), (l, int(cc.max()))
+        assert k < n
+        A = sp.csr_matrix((fine["omega"].astype(np.float64), fine["col"], fine["row_ptr"]), shape=(n, n))
+        Pm = sp.csr_matrix((np.ones(n), (np.arange(n), P)), shape=(n, k))
+        C = (Pm.T @ A @ Pm).tocsr()
+        C.setdiag(0)
+        C.eliminate_zeros()
+        C.sort_indices()
+        np.testing.assert_array_equal(C.indptr, coarse["row_ptr"])
+        np.testing.assert_array_equal(C.indices, coarse["col"])
+        np.testing.assert_array_equal(C.data.astype(np.int64), coarse["omega"].astype(np.int64))
+
+
 @pytest.mark.parametrize("name", ["cfg3_mesh64", "cfg5_grid16", "cfg4_cl20000", "cfg3", "cfg4"])
 def test_sclap_hierarchy_bitwise(mm, name):
-    """SCLaP (R6) on the GPU vs the oracle: every level identical."""
+    """SCLaP on the GPU vs the oracle's implementation of the same synchronous
+    reading R6: every level identical.  The paper's sequential
+    rule (R6s) is the oracle for validity and quality
+    (tests/test_oracle_hierarchy.py::test_sclap_synchronous_reading_quality_vs_paper_rule)."""
     import oracle
 
     w = workload(name)

@@ -260,3 +260,116 @@ def test_sclap_size_bound_blocks_merge():
     lab = oracle.sclap_labels(g, U=2, rounds=5, seed=1, level=0)
     assert np.bincount(lab).max() <= 2
     assert lab[1] == 0  # node 1 moves to the smaller label 0 in round 0
+
+
+# ---------------------------------------------------------------- SCLaP, the paper's sequential rule (R6s)
+def _two_cliques(k):
+    u, v = [], []
+    for base in (0, k):
+        for a in range(k):
+            for b in range(a + 1, k):
+                u.append(base + a)
+                v.append(base + b)
+    u.append(k - 1)
+    v.append(k)  # the bridge
+    return graphs.from_edges(2 * k, np.array(u), np.array(v))
+
+
+def test_sclap_seq_two_cliques():
+    """P:206-209: "nodes in a dense cluster usually agree on a common label":
+    two K6 joined by one edge, U = 6 (a clique fits exactly), one label per
+    clique whatever the random order (several seeds)."""
+    g = _two_cliques(6)
+    for seed in range(8):
+        lab = oracle.sclap_labels(g, U=6, rounds=5, seed=seed, level=0, seq=True)
+        assert len(set(lab[:6].tolist())) == 1 and len(set(lab[6:].tolist())) == 1, (seed, lab)
+        assert lab[0] != lab[6]
+
+
+def test_sclap_seq_bound_and_conservation():
+    """every cluster weighs <= U after every label change; the
+    weights of the nodes are conserved (labels partition the nodes)."""
+    w = configs.make("cfg3_mesh32")
+    rng = np.random.default_rng(3)
+    c = rng.integers(1, 4, w.n).astype(np.int64)
+    for U in (3, 5, 9):
+        lab = oracle.sclap_labels(w.graph, U=U, rounds=4, seed=7, level=1, c=c, seq=True)
+        cw = np.bincount(lab, weights=c, minlength=w.n)
+        assert cw.max() <= U and cw.sum() == c.sum()
+
+
+def test_sclap_seq_no_room_no_move():
+    """U = max c: no cluster can take another node, so no label changes."""
+    w = configs.make("cfg3_mesh32")
+    lab = oracle.sclap_labels(w.graph, U=1, rounds=3, seed=1, level=0, seq=True)
+    assert np.array_equal(lab, np.arange(w.n))
+
+
+def test_sclap_seq_predominant_label_at_the_end():
+    """A fixed point of the rule: after a round without moves, no node has an
+    admissible label (not overloaded after the change) with a strictly larger
+    edge weight than its own cluster's."""
+    w = configs.make("cfg3_mesh32")
+    U = 4
+    lab = oracle.sclap_labels(w.graph, U=U, rounds=200, seed=5, level=0, seq=True)
+    cw = np.bincount(lab, minlength=w.n)
+    rp, col = w.graph.row_ptr, w.graph.col
+    for v in range(w.n):
+        sc = {}
+        for j in col[rp[v]:rp[v + 1]]:
+            sc[lab[j]] = sc.get(lab[j], 0) + 1
+        own = sc.get(lab[v], 0)
+        for L, s in sc.items():
+            if L != lab[v] and cw[L] + 1 <= U:
+                assert s <= own, (v, L, s, own)
+
+
+def test_sclap_seq_immediate_updates_differ_from_synchronous():
+    """The sequential rule sees moves made earlier in the same round (P:207
+    "visits all nodes ... and assigns"), the synchronous reading R6 does not:
+    on a long path with a large U one sequential round already forms clusters
+    of more than two nodes, which one R6 round cannot (each node moves at most
+    once, to a label that was a singleton at the start of the round)."""
+    g = H.path(200)
+    seq = oracle.sclap_labels(g, U=50, rounds=1, seed=3, level=0, seq=True)
+    syn = oracle.sclap_labels(g, U=50, rounds=1, seed=3, level=0)
+    assert np.bincount(seq).max() > 2
+    assert np.bincount(syn).max() <= 2
+
+
+@pytest.mark.parametrize("name", ["cfg3_mesh64", "cfg5_grid16", "cfg4_cl20000"])
+def test_sclap_seq_hierarchy_invariants(name):
+    """The paper's SCLaP hierarchy (R6s): U bound per level, conservation."""
+    w = configs.make(name)
+    lv = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=100, sclap=True, sclap_seq=True)
+    assert len(lv) >= 3
+    for l in range(len(lv) - 1):
+        fine, coarse = lv[l], lv[l + 1]
+        np.testing.assert_array_equal(np.bincount(fine.parent, weights=fine.c, minlength=coarse.n).astype(np.int64),
+                                      coarse.c)
+        assert coarse.c.max() <= max(int(fine.c.max()), int(2.0 ** (l + 1)))
+
+
+def test_sclap_synchronous_reading_quality_vs_paper_rule():
+    """The synchronous reading R6 (what the GPU runs) against the paper's
+    sequential rule on the same graphs: both coarsen geometrically to the
+    stop size, R6 within a few levels of the sequential hierarchy, and the
+    paper's full optimizer (SCLaP + disc prolongation + alpha schedule, h = 2)
+    reaches a final maxent-stress energy of the same quality (geometric mean
+    ratio within [2/3, 3/2] over the instances)."""
+    ratios = []
+    for name in ("cfg3_mesh64", "cfg5_grid12", "cfg3_mesh128"):
+        w = configs.make(name)
+        lr = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=100, sclap=True)
+        ls = oracle.build_hierarchy(w.graph, seed=w.seed, n_stop=100, sclap=True, sclap_seq=True)
+        assert lr[-1].n <= 100 and ls[-1].n <= 100
+        assert abs(len(lr) - len(ls)) <= 3, ([l.n for l in lr], [l.n for l in ls])
+        for fine, coarse in zip(lr[:-1], lr[1:]):
+            assert coarse.n <= 0.9 * fine.n
+        sched = oracle.paper_schedule(max_final_iters=30)
+        e = [oracle.layout_schedule(w.graph, w.S, w.dim, w.q, 2, sched, w.seed, n_stop=100, sclap=True, disc=True,
+                                    sclap_seq=s)[1][2] for s in (False, True)]
+        assert e[0] > 0 and e[1] > 0
+        ratios.append(e[0] / e[1])
+    g = float(np.exp(np.mean(np.log(ratios))))
+    assert 2.0 / 3.0 <= g <= 1.5, ratios

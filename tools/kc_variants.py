@@ -64,10 +64,21 @@ def time_one(name, lib):
         torch.cuda.synchronize()
         p = mm.profile_read()
         mm.profile_enable(False)
-        ts.append(p["repulse_coarse"]["total_ms"] / p["repulse_coarse"]["launches"])
-    ms = sorted(ts)[1]
-    print(json.dumps({"lib": os.path.basename(lib), "config": name, "n": w.n, "k": k, "ms": ms,
-                      "pairs_per_s": w.n * (k - 1) / (ms / 1e3), "all_ms": ts}), flush=True)
+        ts.append({kk: v["total_ms"] / v["launches"] for kk, v in p.items()})
+    ts.sort(key=lambda t: t["repulse_coarse"])
+    med = ts[1]
+    ms = med["repulse_coarse"]
+    # kernel (a) / (d) algorithmic bytes: 4(n+1) + 12 nnz + 3 b_x n; (b_x + 4) n + b_x k
+    bx = 8 if w.dim == 2 else 16
+    ga = 4 * (w.n + 1) + 12 * w.S.nnz + 3 * bx * w.n
+    ce = (bx + 4) * w.n + bx * k
+    out = {"lib": os.path.basename(lib), "config": name, "n": w.n, "k": k, "nnz": int(w.S.nnz), "ms": ms,
+           "pairs_per_s": w.n * (k - 1) / (ms / 1e3), "kernels_ms": med}
+    if "gather_update" in med:
+        out["gather_GBps"] = ga / (med["gather_update"] * 1e-3) / 1e9
+    if "centroid" in med:
+        out["centroid_GBps"] = ce / (med["centroid"] * 1e-3) / 1e9
+    print(json.dumps(out), flush=True)
 
 
 if __name__ == "__main__":
