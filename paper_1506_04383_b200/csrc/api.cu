@@ -19,6 +19,7 @@
 #include "k_fullstress.cuh"
 #include "k_hier.cuh"
 #include "k_small.cuh"
+#include "k_perm.cuh"
 #include "k_sclap.cuh"
 #include "k_repulse.cuh"
 
@@ -230,6 +231,9 @@ struct SweepBufs {
     uint64_t* rkey = nullptr;    // [2k] representative sort keys (scratch)
     uint32_t* box = nullptr;     // [8] layout box (scratch)
     float4* frame = nullptr;     // [1] kernel (c)'s frame origin (Q28)
+    int32_t* sib = nullptr;      // renumbered level: per-vertex sibling (k_perm.cuh), else NULL
+    int2* sbound = nullptr;      // member range of the rep at each slot (written with the orders)
+    bool contig = false;         // renumbered level: members of a rep are a contiguous range (mem = identity)
     bool reorder = false;        // recompute kernel (c)'s orders before every sweep
     bool far = false;            // kernel (c) with per-sweep frame and tile boxes (lo-free far tiles, Q27/Q28)
     void* tmp = nullptr;
@@ -285,7 +289,7 @@ size_t sweep_bytes(int32_t n, int dim, int32_t k, bool approx, double mean_row) 
         b += 2 * al((size_t)k * sizeof(float4)) + al((size_t)(k + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)(n + 1) * 4) + al((size_t)n * 4);
         b += al((size_t)n * 4) * 2 + al((size_t)(std::max(n, k) + 2) * 4);
-        b += 2 * al((size_t)k * 4) + al((size_t)(k / kCoarseTile + 1) * 4);
+        b += 2 * al((size_t)k * 4) + al((size_t)k * 8) + al((size_t)(k / kCoarseTile + 1) * 4);
         b += 2 * al((size_t)n * 4) + al((size_t)(k / kCoarseTile + 1) * 32) + al((size_t)k * 16) + al(32) + al(16);
         b += al(cub_tmp_bytes(n));
     }
@@ -311,6 +315,7 @@ bool carve_sweep(Carver& cv, int32_t n, int dim, int32_t k, bool approx, double 
         sb.iota = cv.take<int32_t>(n);
         sb.cnt = cv.take<int32_t>(std::max(n, k) + 2);
         sb.rord = cv.take<int32_t>(k);
+        sb.sbound = cv.take<int2>(k);
         sb.rpos = cv.take<int32_t>(k);
         sb.tile_nu = cv.take<int32_t>(k / kCoarseTile + 1);
         sb.tperm = cv.take<int32_t>(n);
@@ -341,10 +346,12 @@ bool far_tiles() {
 // iota = 0..n-1 (k <= n); cnt / key_sorted are free scratch after prepare_approx.
 cudaError_t coarse_orders(int32_t n, int dim, const mm_approx* ap, const float* x, const SweepBufs& sb,
                           cudaStream_t st) {
-    return approx_orders(dim, n, ap->k, sb.mptr, sb.mem, x, kCoarseTile, sb.iota, sb.box, sb.frame, sb.rep_hi,
+    return approx_orders(dim, n, ap->k, sb.mptr, sb.contig ? nullptr : sb.mem, x, kCoarseTile, sb.iota, sb.box,
+                         sb.frame, sb.rep_hi,
                          sb.rep_lo, reinterpret_cast<uint32_t*>(sb.cnt), reinterpret_cast<uint32_t*>(sb.key_sorted),
                          sb.tperm,
-                         sb.tpos, sb.rkey, sb.rkey + ap->k, sb.rord, sb.rpos, sb.tile_nu, sb.tmp, sb.tmp_bytes, st);
+                         sb.tpos, sb.rkey, sb.rkey + ap->k, sb.rord, sb.rpos, sb.tile_nu, sb.tmp, sb.tmp_bytes, st,
+                         sb.contig ? sb.sbound : nullptr);
 }
 
 // Re-sort before every sweep when kernel (c)'s work (n k pairs) dwarfs the two
@@ -368,6 +375,24 @@ double far_min_pairs() {
     return thr;
 }
 
+// Locality renumbering of an Eq.(3) level on the tiled path (k_perm.cuh;
+// MM_RENUMBER=0 disables it: experiments, A/B)
+// mode 1: representative-slot order (members contiguous); 2: Morton order of
+// the level's starting positions (kernel (c)'s target order)
+int renumber_mode() {
+    static const int m = [] {
+        const char* v = getenv("MM_RENUMBER");
+        return v ? atoi(v) : 1;
+    }();
+    return m;
+}
+bool renumber_enabled() { return renumber_mode() != 0; }
+
+size_t renumber_bytes(int32_t n, int64_t nnz, int32_t k) {
+    return 6 * al((size_t)n * 4) + 2 * al((size_t)(k + 1) * 4) + al((size_t)(n + 1) * 8) + 3 * al((size_t)nnz * 4) +
+           al(perm_scan_tmp_bytes((int64_t)std::max(n, k) + 1)) + 1024;
+}
+
 // Group maps into CSRs (members of each representative, children of each parent).
 cudaError_t prepare_approx(int32_t n, int dim, const mm_approx* ap, const float* x, SweepBufs& sb, cudaStream_t st) {
     cudaError_t e = group_by_key(n, ap->ancestor, ap->k, sb.mptr, sb.mem, sb.key_sorted, sb.iota, sb.cnt, sb.tmp,
@@ -387,7 +412,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     const int32_t n = S->n;
     const double mean_row = (double)S->nnz / (double)n;
     const bool qpow = q != 0.0f;
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     RepulsePlan p;
     SymPlan sp;
     if (ap) {
@@ -396,8 +421,9 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
         else if (sb.far) e = launch_frame_fused(dim, n, x_in, sb.box, sb.frame, st);
         if (e != cudaSuccess) return e;
         const float4* frame = sb.far ? sb.frame : nullptr;
-        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.mem, x_in, sb.rord, frame, sb.rep_hi, sb.rep_lo,
-                            sb.far ? sb.tile_box : nullptr, kCoarseTile, st);
+        e = launch_centroid(dim, n, ap->k, sb.mptr, sb.contig ? nullptr : sb.mem, x_in, sb.rord, frame, sb.rep_hi,
+                            sb.rep_lo, sb.far ? sb.tile_box : nullptr, kCoarseTile, st,
+                            sb.contig ? sb.sbound : nullptr);
         if (e != cudaSuccess) return e;
         p = plan_repulse(n, ap->k, dim, true, qpow);
         CoarseOrder co;
@@ -444,6 +470,7 @@ cudaError_t sweep_core(const mm_sset* S, int dim, float alpha, float q, const mm
     ga.parent = ap ? ap->parent : nullptr;
     ga.child_ptr = ap ? sb.cptr : nullptr;
     ga.child = ap ? sb.child : nullptr;
+    ga.sib = ap ? sb.sib : nullptr;
     ga.x_out = x_out;
     ga.stat_partial = sb.stat_partial;
     ga.flags = sb.flags;
@@ -1644,6 +1671,20 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
             wsb = std::max(wsb, sweep_bytes(H->lv[l].n, dim, k, hp > 0, 1.0));
         }
         const size_t need = wsb + 2 * al(xbytes) + 2 * al((size_t)n0 * 4) + al(sizeof(mm_sweep_stats)) + al(64);
+        // locality renumbering of the Eq.(3) levels that run on the tiled path
+        size_t rnb = 0;
+        if (renumber_enabled()) {
+            for (int32_t l = lo_level; l <= hi_level; ++l) {
+                const int32_t hp = std::min(h, L - l);
+                if (hp <= 0) continue;
+                const int32_t k = H->lv[l + hp].n;
+                if (small_level_ok(dim, H->lv[l].n, k, true)) continue;
+                const int64_t nnz_l = l == 0 ? S->nnz : H->lv[l].nnz;
+                rnb = std::max(rnb, renumber_bytes(H->lv[l].n, nnz_l, k));
+            }
+        }
+        DevBuf rbuf(rnb, ls);
+        if (rnb && !rbuf.p) { set_err("%s: out of device memory (%zu B)", who, rnb); return MM_ERR_OUT_OF_MEMORY; }
         DevBuf buf(need, ls);
         if (!buf.p) { set_err("%s: out of device memory (%zu B)", who, need); return MM_ERR_OUT_OF_MEMORY; }
         Carver cv(buf.p, need);
@@ -1703,9 +1744,61 @@ mm_status layout_impl(const mm_graph* g, const mm_sset* S, int dim, float q, int
             float* other = (cur == xa) ? xb : xa;
             const float* res = nullptr;
             int32_t nsw = 0;
-            if ((s = run.run(&Sl, dim, q, app, cur, other, (float*)cur, dstats, sbl, ls, l, dynamic, &res, &nsw)) !=
-                MM_OK)
+            const bool renum = app && rnb > 0 && !small_level_ok(dim, nf, ap.k, true);
+            if (renum) {
+                // vertices in representative-slot order (k_perm.cuh): permute S^l, the
+                // maps and x, redo the maps / orders there, sweep, scatter x back
+                Carver rc(rbuf.p, rnb);
+                int32_t* perm = rc.take<int32_t>(nf);
+                int32_t* inv = rc.take<int32_t>(nf);
+                int32_t* anc_r = rc.take<int32_t>(nf);
+                int32_t* par_r = rc.take<int32_t>(nf);
+                int32_t* sib = rc.take<int32_t>(nf);
+                int32_t* len = rc.take<int32_t>(nf);
+                int32_t* cnt = rc.take<int32_t>(ap.k + 1);
+                int32_t* sptr = rc.take<int32_t>(ap.k + 1);
+                int64_t* rp_r = rc.take<int64_t>((size_t)nf + 1);
+                int32_t* col_r = rc.take<int32_t>((size_t)Sl.nnz);
+                float* d_r = rc.take<float>((size_t)Sl.nnz);
+                float* w_r = rc.take<float>((size_t)Sl.nnz);
+                void* stmp = rc.take<char>(perm_scan_tmp_bytes((int64_t)std::max(nf, ap.k) + 1));
+                if (!rc.ok) { set_err("%s: renumber carving failed", who); return MM_ERR_INVALID_ARGUMENT; }
+                if (renumber_mode() == 2) {
+                    MM_CU(cudaMemcpyAsync(perm, sbl.tperm, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, ls), "renumber");
+                    MM_CU(cudaMemcpyAsync(inv, sbl.tpos, 4 * (size_t)nf, cudaMemcpyDeviceToDevice, ls), "renumber");
+                    MM_CU(gather_i32(nf, perm, ap.ancestor, anc_r, ls), "mm_layout renumber");
+                } else {
+                    MM_CU(level_perm(ap.k, sbl.rord, sbl.mptr, sbl.mem, cnt, sptr, perm, inv, anc_r, stmp, ls),
+                          "mm_layout renumber");
+                }
+                MM_CU(permute_sset(nf, Sl.row_ptr, Sl.col, Sl.d, Sl.w, perm, inv, rp_r, col_r, d_r, w_r, len, stmp, ls),
+                      "mm_layout renumber");
+                MM_CU(gather_i32(nf, perm, ap.parent, par_r, ls), "mm_layout renumber");
+                MM_CU(permute_x(dim, nf, perm, cur, other, false, ls), "mm_layout renumber");
+                mm_sset Sr = Sl;
+                Sr.row_ptr = rp_r;
+                Sr.col = col_r;
+                Sr.d = d_r;
+                Sr.w = w_r;
+                mm_approx apr;
+                apr.k = ap.k;
+                apr.parent = par_r;
+                apr.ancestor = anc_r;
+                // members of every representative are now one contiguous range (mem = identity)
+                sbl.contig = renumber_mode() != 2;
+                MM_CU(prepare_approx(nf, dim, &apr, other, sbl, ls), "mm_layout prepare_approx");
+                MM_CU(sibling_of(nf, sbl.cptr, sbl.child, sib, ls), "mm_layout renumber");
+                sbl.sib = sib;
+                if ((s = run.run(&Sr, dim, q, &apr, other, (float*)cur, other, dstats, sbl, ls, l, dynamic, &res,
+                                 &nsw)) != MM_OK)
+                    return s;
+                float* back = (res == cur) ? other : (float*)cur;
+                MM_CU(permute_x(dim, nf, perm, res, back, true, ls), "mm_layout renumber");
+                res = back;
+            } else if ((s = run.run(&Sl, dim, q, app, cur, other, (float*)cur, dstats, sbl, ls, l, dynamic, &res,
+                                    &nsw)) != MM_OK) {
                 return s;
+            }
             if (trace_on()) {
                 char msg[160];
                 snprintf(msg, sizeof(msg), "layout: level %d done (n %d, k %d, %d sweeps enqueued)", l, nf,

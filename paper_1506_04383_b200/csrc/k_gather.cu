@@ -68,6 +68,63 @@ constexpr int kGatherUnroll = MM_GATHER_UNROLL;
 #ifndef MM_GATHER_UNROLL_G1
 #define MM_GATHER_UNROLL_G1 2  // one lane per vertex (short rows, e.g. cfg5's 6): unroll 2 measured +10% there (tools/gpu_session87.sh)
 #endif
+// fixed-order block reduction of (dx2, x2, stress); the last CTA to finish
+// reduces the per-CTA partials in CTA order and re-arms the ticket and flags
+__device__ __forceinline__ void gather_finish_stats(const GatherArgs& a, double v_dx2, double v_x2, double v_st) {
+    __shared__ double red[3][kGBlock / 32];
+    __shared__ bool last;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        v_dx2 += __shfl_xor_sync(0xffffffffu, v_dx2, o);
+        v_x2 += __shfl_xor_sync(0xffffffffu, v_x2, o);
+        v_st += __shfl_xor_sync(0xffffffffu, v_st, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[0][threadIdx.x >> 5] = v_dx2;
+        red[1][threadIdx.x >> 5] = v_x2;
+        red[2][threadIdx.x >> 5] = v_st;
+    }
+    __syncthreads();
+    if (threadIdx.x < 3) {
+        double s = 0.0;
+        for (int w = 0; w < kGBlock / 32; ++w) s += red[threadIdx.x][w];
+        a.stat_partial[(int64_t)blockIdx.x * 3 + threadIdx.x] = s;
+        __threadfence();  // each writer publishes its own partial before the ticket
+    }
+    __syncthreads();
+    // last CTA to finish reduces the per-CTA partials in CTA order (the order
+    // does not depend on which CTA is last) and re-arms the ticket and flags
+    if (threadIdx.x == 0) last = atomicAdd(a.ticket, 1) == (int)gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double t[3] = {0.0, 0.0, 0.0};
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += kGBlock)
+        for (int k = 0; k < 3; ++k) t[k] += __ldcg(a.stat_partial + (int64_t)b * 3 + k);
+    for (int k = 0; k < 3; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t[k] += __shfl_xor_sync(0xffffffffu, t[k], o);
+    }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0)
+        for (int k = 0; k < 3; ++k) red[k][threadIdx.x >> 5] = t[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double tot[3] = {0.0, 0.0, 0.0};
+        for (int w = 0; w < kGBlock / 32; ++w)
+            for (int k = 0; k < 3; ++k) tot[k] += red[k][w];
+        const int32_t fl = atomicExch(a.flags, 0);
+        if (a.stats) {
+            a.stats->dx2 = tot[0];
+            a.stats->x2 = tot[1];
+            a.stats->stress = 0.5 * tot[2];
+            a.stats->flags = fl;
+            a.stats->pad = 0;
+        }
+        *a.ticket = 0;
+    }
+}
+
 template <int DIM, bool QPOW, int G>
 __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a, float cexp) {
     if (a.alpha_dev) a.alpha = (float)*a.alpha_dev;  // same rounding as the host path's (float)alpha
@@ -79,14 +136,15 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
     // which takes one level off each dependent chain (rp -> col -> x[col],
     // parent -> child_ptr -> child -> x, anc -> rpos -> rep, tpos -> partials)
     int64_t nx_e0 = 0, nx_e1 = 0;
-    int32_t nx_tp = 0, nx_par = 0, nx_anc = 0;
+    int32_t nx_tp = 0, nx_par = 0, nx_anc = 0, nx_sib = -1;
     auto prefetch = [&](int64_t vb2) {
         const int64_t i2 = vb2 + threadIdx.x / G;
         if (MM_GATHER_PREFETCH && i2 < a.n) {
             nx_e0 = a.rp[i2];
             nx_e1 = a.rp[i2 + 1];
             if (a.tpos != nullptr) nx_tp = __ldg(a.tpos + i2);
-            if (a.parent != nullptr) nx_par = __ldg(a.parent + i2);
+            if (a.sib != nullptr) nx_sib = __ldg(a.sib + i2);
+            else if (a.parent != nullptr) nx_par = __ldg(a.parent + i2);
             if (a.anc != nullptr) nx_anc = __ldg(a.anc + i2);
         }
     };
@@ -97,7 +155,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
         const int64_t i = vb + threadIdx.x / G;
         const bool valid = i < a.n;
         const int64_t cur_e0 = nx_e0, cur_e1 = nx_e1;
-        const int32_t cur_tp = nx_tp, cur_par = nx_par, cur_anc = nx_anc;
+        const int32_t cur_tp = nx_tp, cur_par = nx_par, cur_anc = nx_anc, cur_sib = nx_sib;
         prefetch(vb + (int64_t)gridDim.x * VPB);
         float4 xi = make_float4(0.f, 0.f, 0.f, 0.f);
         float rho = 0.f, st = 0.f;
@@ -200,8 +258,14 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 C.y = fmaf(dy, inv, C.y);
                 if constexpr (DIM == 3) C.z = fmaf(dz, inv, C.z);
             }
-            if (a.parent != nullptr) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
-                const int32_t p = MM_GATHER_PREFETCH ? cur_par : __ldg(a.parent + i);
+            int32_t sb = -2;
+            if (a.sib != nullptr) {
+                sb = MM_GATHER_PREFETCH ? cur_sib : __ldg(a.sib + i);
+                // the only sibling (matching hierarchies): one term, as the child walk below
+                if (sb >= 0 && lg == 0) r_value<DIM, QPOW>(xi, load_x<DIM>(a.x, sb), cexp, C, -1.f);
+            }
+            if (a.parent != nullptr && sb == -2) {  // Eq.(3): same-cluster exact r-values (added: sign -1 on C)
+                const int32_t p = (MM_GATHER_PREFETCH && a.sib == nullptr) ? cur_par : __ldg(a.parent + i);
                 const int32_t c0 = __ldg(a.child_ptr + p), c1 = __ldg(a.child_ptr + p + 1);
                 for (int32_t c = c0 + lg; c < c1; c += G) {
                     const int32_t j = __ldg(a.child + c);
@@ -241,60 +305,7 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
             v_st += (double)st;
         }
     }
-    // fixed-order block reduction of (dx2, x2, stress)
-    __shared__ double red[3][kGBlock / 32];
-    __shared__ bool last;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        v_dx2 += __shfl_xor_sync(0xffffffffu, v_dx2, o);
-        v_x2 += __shfl_xor_sync(0xffffffffu, v_x2, o);
-        v_st += __shfl_xor_sync(0xffffffffu, v_st, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = v_dx2;
-        red[1][threadIdx.x >> 5] = v_x2;
-        red[2][threadIdx.x >> 5] = v_st;
-    }
-    __syncthreads();
-    if (threadIdx.x < 3) {
-        double s = 0.0;
-        for (int w = 0; w < kGBlock / 32; ++w) s += red[threadIdx.x][w];
-        a.stat_partial[(int64_t)blockIdx.x * 3 + threadIdx.x] = s;
-    }
-    // last CTA to finish reduces the per-CTA partials in CTA order (the order
-    // does not depend on which CTA is last) and re-arms the ticket and flags
-    if (threadIdx.x == 0) {
-        __threadfence();
-        last = atomicAdd(a.ticket, 1) == (int)gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-    double t[3] = {0.0, 0.0, 0.0};
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += kGBlock)
-        for (int k = 0; k < 3; ++k) t[k] += __ldcg(a.stat_partial + (int64_t)b * 3 + k);
-    for (int k = 0; k < 3; ++k) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) t[k] += __shfl_xor_sync(0xffffffffu, t[k], o);
-    }
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0)
-        for (int k = 0; k < 3; ++k) red[k][threadIdx.x >> 5] = t[k];
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double tot[3] = {0.0, 0.0, 0.0};
-        for (int w = 0; w < kGBlock / 32; ++w)
-            for (int k = 0; k < 3; ++k) tot[k] += red[k][w];
-        const int32_t fl = atomicExch(a.flags, 0);
-        if (a.stats) {
-            a.stats->dx2 = tot[0];
-            a.stats->x2 = tot[1];
-            a.stats->stress = 0.5 * tot[2];
-            a.stats->flags = fl;
-            a.stats->pad = 0;
-        }
-        *a.ticket = 0;
-    }
+    gather_finish_stats(a, v_dx2, v_x2, v_st);
 }
 
 __global__ void k_stats_final(const double* __restrict__ partial, int nblocks, const int32_t* __restrict__ flags,

@@ -318,21 +318,29 @@ __global__ void k_compose(int32_t n, const int32_t* __restrict__ a, const int32_
 // representative (G from the mean cluster size: 2 at h = 2, 32 at h = 7):
 // lane l sums members l, l+G, ... in order, then a fixed shuffle tree.
 template <int DIM, int G>
+// mem == nullptr: members are the contiguous ranges themselves (renumbered
+// level, k_perm.cuh); sbound (nullable): the member range of each slot
 __global__ void k_centroid(int32_t k, const int32_t* __restrict__ mptr, const int32_t* __restrict__ mem,
                            const float* __restrict__ x, const int32_t* __restrict__ rord,
                            const float4* __restrict__ frame, float4* __restrict__ rep_hi,
-                           float4* __restrict__ rep_lo) {
+                           float4* __restrict__ rep_lo, const int2* __restrict__ sbound) {
     const int64_t tg = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int32_t slot = (int32_t)(tg / G);
-    const int32_t v = (rord != nullptr && slot < k) ? __ldg(rord + slot) : slot;
     const int lg = (int)(tg & (G - 1));
     double sx = 0.0, sy = 0.0, sz = 0.0;
     int32_t b = 0, e = 0;
-    if (v < k) {
-        b = mptr[v];
-        e = mptr[v + 1];
+    if (slot < k) {
+        if (sbound != nullptr) {
+            const int2 be = __ldg(sbound + slot);
+            b = be.x;
+            e = be.y;
+        } else {
+            const int32_t v = rord != nullptr ? __ldg(rord + slot) : slot;
+            b = mptr[v];
+            e = mptr[v + 1];
+        }
         for (int32_t t = b + lg; t < e; t += G) {
-            const float4 p = load_x<DIM>(x, __ldg(mem + t));
+            const float4 p = load_x<DIM>(x, mem != nullptr ? __ldg(mem + t) : t);
             sx += p.x;
             sy += p.y;
             sz += p.z;
@@ -512,11 +520,16 @@ __global__ void k_rep_keys_c(int32_t k, const int32_t* __restrict__ mptr, const 
     key[v] = ((uint64_t)(uint32_t)(mptr[v + 1] - mptr[v]) << 32) | morton_key<DIM>(p, box);
 }
 // rpos = inverse of rord; tile_nu[t] = the common mass of slots [tile t, tile t + tile - 1] or 0
+// sbound (nullable): member range [mptr[r], mptr[r+1]) of the rep at each slot, so
+// that the centroid refresh reads it coalesced
 __global__ void k_rep_slots(int32_t k, const int32_t* __restrict__ rord, const uint64_t* __restrict__ key_sorted,
-                            int32_t* __restrict__ rpos, int32_t* __restrict__ tile_nu, int tile) {
+                            int32_t* __restrict__ rpos, int32_t* __restrict__ tile_nu, int tile,
+                            const int32_t* __restrict__ mptr, int2* __restrict__ sbound) {
     const int32_t s = blockIdx.x * blockDim.x + threadIdx.x;
     if (s >= k) return;
-    rpos[rord[s]] = s;
+    const int32_t r = rord[s];
+    rpos[r] = s;
+    if (sbound != nullptr) sbound[s] = make_int2(mptr[r], mptr[r + 1]);
     if (s % tile == 0) {
         const int32_t last = min(s + tile - 1, k - 1);
         const uint32_t a = (uint32_t)(key_sorted[s] >> 32), b = (uint32_t)(key_sorted[last] >> 32);
@@ -889,7 +902,7 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
                           int tile, const int32_t* iota, uint32_t* box, float4* frame, float4* rep_hi,
                           float4* rep_lo, uint32_t* tkey, uint32_t* tkey_sorted, int32_t* tperm, int32_t* tpos,
                           uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord, int32_t* rpos, int32_t* tile_nu,
-                          void* tmp, size_t tmp_bytes, cudaStream_t st) {
+                          void* tmp, size_t tmp_bytes, cudaStream_t st, int2* sbound) {
     if (k <= 0 || n <= 0) return cudaSuccess;
     cudaError_t e = launch_frame(dim, n, x, box, frame, st);
     if (e != cudaSuccess) return e;
@@ -916,17 +929,17 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
     }
     LaunchScope ls("order_slots", st);
     k_scatter_inv<<<nblk(n), 256, 0, st>>>(n, tperm, tpos);
-    k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, rkey_sorted, rpos, tile_nu, tile);
+    k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, rkey_sorted, rpos, tile_nu, tile, mptr, sbound);
     k_box_init<<<1, 32, 0, st>>>(box);  // armed for launch_frame_fused
     return cudaGetLastError();
 }
 
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
                             const int32_t* rord, const float4* frame, float4* rep_hi, float4* rep_lo,
-                            float4* tile_box, int tile, cudaStream_t st) {
+                            float4* tile_box, int tile, cudaStream_t st, const int2* sbound) {
     if (tile_box != nullptr && k > 0) {
         const cudaError_t e = launch_centroid(dim, n, k, mptr, mem, x, rord, frame, rep_hi, rep_lo, nullptr, tile,
-                                              st);
+                                              st, sbound);
         if (e != cudaSuccess) return e;
         LaunchScope ls("tile_box", st);
         const int nt = (k + tile - 1) / tile;
@@ -942,12 +955,12 @@ cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, 
     const int nb = nblk((int64_t)k * G);
 #define MM_C(D)                                                                               \
     switch (G) {                                                                              \
-        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
-        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
-        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
-        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break;   \
-        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break; \
-        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo); break; \
+        case 1: k_centroid<D, 1><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo, sbound); break;   \
+        case 2: k_centroid<D, 2><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo, sbound); break;   \
+        case 4: k_centroid<D, 4><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo, sbound); break;   \
+        case 8: k_centroid<D, 8><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo, sbound); break;   \
+        case 16: k_centroid<D, 16><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo, sbound); break; \
+        default: k_centroid<D, 32><<<nb, 256, 0, st>>>(k, mptr, mem, x, rord, frame, rep_hi, rep_lo, sbound); break; \
     }
     if (dim == 2) { MM_C(2) } else { MM_C(3) }
 #undef MM_C

@@ -48,13 +48,15 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
                           int tile, const int32_t* iota, uint32_t* box, float4* frame, float4* rep_hi,
                           float4* rep_lo, uint32_t* tkey, uint32_t* tkey_sorted, int32_t* tperm, int32_t* tpos,
                           uint64_t* rkey, uint64_t* rkey_sorted, int32_t* rord, int32_t* rpos, int32_t* tile_nu,
-                          void* tmp, size_t tmp_bytes, cudaStream_t st);
+                          void* tmp, size_t tmp_bytes, cudaStream_t st, int2* sbound = nullptr);
 // rord nullable: representative v at slot v; else rep rord[s] is written at slot s.
+// mem nullable: the members of a representative are the contiguous range itself
+// (renumbered level); sbound nullable: else the member range of each slot.
 // frame nullable: coordinates relative to the origin *frame (Q28).
 // tile_box nullable: else the box of every `tile` slots is written (kernel (c)'s skip test, Q27)
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
                             const int32_t* rord, const float4* frame, float4* rep_hi, float4* rep_lo,
-                            float4* tile_box, int tile, cudaStream_t st);
+                            float4* tile_box, int tile, cudaStream_t st, const int2* sbound = nullptr);
 cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
                            int32_t level, float* x, cudaStream_t st);
 cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,

@@ -117,6 +117,9 @@ struct GatherArgs {
     const int32_t* parent;
     const int32_t* child_ptr;
     const int32_t* child;
+    // nullable: per-vertex sibling (>= 0: the only other child of its parent;
+    // -1: none; -2: larger family, walk child_ptr/child) from the renumbered level
+    const int32_t* sib = nullptr;
     float* x_out;
     double* stat_partial; // [nblocks][3]
     int32_t* flags;       // device int (OR-ed); re-armed to 0 by the last CTA

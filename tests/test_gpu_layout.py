@@ -121,10 +121,11 @@ def test_layout_exact_rgg_full_run(mm):
 
 
 @pytest.mark.parametrize("name,n_stop", [("cfg3_mesh64", 200), ("cfg5_grid16", 200), ("cfg4_cl20000", 1000),
-                                         ("cfg3_mesh128", 1000)])
+                                         ("cfg3_mesh128", 1000), ("cfg3_mesh256", 1000), ("cfg5_grid40", 1000)])
 def test_layout_multilevel_full_run(mm, name, n_stop):
     """Multilevel runs (h = 2, per-level sweeps of the config) on scaled-down
-    instances of configs[2..4]'s generators."""
+    instances of configs[2..4]'s generators; mesh256 and grid40 have finest
+    levels above the persistent-kernel limit, so they run renumbered (k_perm)."""
     w = workload(name)
     g = mm.graph_to_device(w.graph)
     S = mm.sset_to_device(w.S)
