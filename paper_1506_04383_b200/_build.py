@@ -10,7 +10,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libmm_b200.so")
 BUILD = os.path.join(HERE, "csrc", "build")
-SOURCES = ["k_repulse.cu", "k_gather.cu", "k_hier.cu", "k_fullstress.cu", "k_sclap.cu", "k_small.cu", "k_perm.cu", "api.cu"]
+SOURCES = ["k_repulse.cu", "k_gather.cu", "k_hier.cu", "k_fullstress.cu", "k_sclap.cu", "k_small.cu", "k_perm.cu", "k_sort.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

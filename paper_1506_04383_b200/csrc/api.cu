@@ -240,6 +240,7 @@ struct SweepBufs {
     size_t tmp_bytes = 0;
 };
 
+// scratch of the hand-written sorts / scans of one sweep's maps and orders
 size_t cub_tmp_bytes(int32_t n) {
     return std::max({sort_temp_bytes_i32(n), sort_temp_bytes_u64(n), scan_temp_bytes(n + 2)}) + 256;
 }

@@ -18,7 +18,8 @@
 // id order from a CSR built by a stable sort, so the FP32 sum is deterministic.
 // Prolongation (Q15, BASELINE.json configs[2]): x_u = x_{P(u)} + 1e-3 (2U - 1)
 // per component, U from the counter RNG keyed (seed, JITTER, level, u*dim+k).
-#include <cub/cub.cuh>
+#include "k_perm.cuh"
+#include "k_sort.cuh"
 
 #include "k_hier.cuh"
 
@@ -757,30 +758,19 @@ cudaError_t launch_fill(int64_t n, int32_t v, int32_t* a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-size_t scan_temp_bytes(int32_t n) {
-    size_t b = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, n);
-    return b;
-}
+// scratch of the hand-written scan / sort (k_perm.cu, k_sort.cu) used below
+size_t scan_temp_bytes(int32_t n) { return perm_scan_tmp_bytes((int64_t)n + 1); }
 
-size_t sort_temp_bytes_u64(int64_t m) {
-    size_t b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, (uint64_t*)nullptr, (uint64_t*)nullptr, (int32_t*)nullptr,
-                                    (int32_t*)nullptr, m);
-    return b;
-}
+size_t sort_temp_bytes_u64(int64_t m) { return radix_sort_tmp_bytes<uint64_t>(m); }
 
-size_t sort_temp_bytes_i32(int32_t n) {
-    size_t b = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, b, (int32_t*)nullptr, (int32_t*)nullptr, (int32_t*)nullptr,
-                                    (int32_t*)nullptr, n);
-    return b;
-}
+size_t sort_temp_bytes_i32(int32_t n) { return radix_sort_tmp_bytes<uint32_t>(n); }
 
+// exclusive sum of n items (out[0..n-1]), as the scans of the contraction need
 cudaError_t exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, void* tmp, size_t tmp_bytes,
                                cudaStream_t st) {
-    LaunchScope ls("cub_scan", st);
-    return cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, in, out, n, st);
+    if (n <= 0) return cudaSuccess;
+    if (tmp_bytes < perm_scan_tmp_bytes(n)) return cudaErrorInvalidValue;
+    return scan_i32_excl<int32_t>(in, out, (int64_t)n - 1, tmp, st);
 }
 
 cudaError_t contract_leaders(int32_t n, const int32_t* mate, const int32_t* c, int32_t* flag, int32_t* cid,
@@ -813,11 +803,8 @@ cudaError_t contract_edges(int32_t n, int64_t nnz, const int64_t* rp, const int3
     const uint64_t sentinel = (uint64_t)nc * (uint64_t)nc;
     int end_bit = 1;
     while (end_bit < 64 && (sentinel >> end_bit) != 0) ++end_bit;
-    {
-        LaunchScope ls("cub_sort_edges", st);
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, keys, keys_alt, vals, vals_alt, nnz, 0, end_bit, st);
-        if (e != cudaSuccess) return e;
-    }
+    e = radix_sort_pairs<uint64_t>(keys, keys_alt, vals, vals_alt, nnz, 0, end_bit, tmp, tmp_bytes, st, "sort_edges");
+    if (e != cudaSuccess) return e;
     {
         LaunchScope ls("run_heads", st);
         k_run_heads<<<nblk(nnz), 256, 0, st>>>(nnz, keys_alt, sentinel, head);
@@ -855,11 +842,10 @@ cudaError_t group_by_key(int32_t n, const int32_t* key, int32_t k, int32_t* ptr,
     }
     int end_bit = 1;
     while (end_bit < 31 && ((k - 1) >> end_bit) != 0) ++end_bit;
-    {
-        LaunchScope ls("cub_sort_group", st);
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, key, key_sorted, iota, members, n, 0, end_bit, st);
-        if (e != cudaSuccess) return e;
-    }
+    // keys are non-negative ids < k: sorted as unsigned
+    e = radix_sort_pairs<uint32_t>(reinterpret_cast<const uint32_t*>(key), reinterpret_cast<uint32_t*>(key_sorted), iota,
+                                   members, n, 0, end_bit, tmp, tmp_bytes, st, "sort_group");
+    if (e != cudaSuccess) return e;
     e = launch_fill(k + 1, 0, cnt, st);
     if (e != cudaSuccess) return e;
     {
@@ -919,14 +905,11 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
             k_rep_keys_c<3><<<nblk(k), 256, 0, st>>>(k, mptr, rep_hi, frame, box, rkey);
         }
     }
-    {
-        LaunchScope ls("cub_sort_order", st);
-        // stable: equal keys keep id order
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, tkey, tkey_sorted, iota, tperm, n, 0, 32, st);
-        if (e != cudaSuccess) return e;
-        e = cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, rkey, rkey_sorted, iota, rord, k, 0, 64, st);
-        if (e != cudaSuccess) return e;
-    }
+    // stable: equal keys keep id order
+    e = radix_sort_pairs<uint32_t>(tkey, tkey_sorted, iota, tperm, n, 0, 32, tmp, tmp_bytes, st, "sort_order");
+    if (e != cudaSuccess) return e;
+    e = radix_sort_pairs<uint64_t>(rkey, rkey_sorted, iota, rord, k, 0, 64, tmp, tmp_bytes, st, "sort_order");
+    if (e != cudaSuccess) return e;
     LaunchScope ls("order_slots", st);
     k_scatter_inv<<<nblk(n), 256, 0, st>>>(n, tperm, tpos);
     k_rep_slots<<<nblk(k), 256, 0, st>>>(k, rord, rkey_sorted, rpos, tile_nu, tile, mptr, sbound);

@@ -47,7 +47,8 @@ def main(name):
             rec.update({"algo_bytes": algo[kern], "GBps": gbs, "frac_hbm": gbs / HBM})
         out[kern.rstrip("<")] = rec
     # one-off per-level work of the finest level (renumbering, orders)
-    for kern in ("k_permute_rows", "k_slot_fill", "k_permute_x", "k_scan_out"):
+    for kern in ("k_permute_rows", "k_slot_fill", "k_permute_x", "k_scan_out", "k_rs_hist", "k_rs_scatter",
+                 "DeviceRadixSort", "k_scan_sums"):
         ts = [e.time_range.elapsed_us() for e in evs if kern in e.name]
         if ts:
             out[kern] = {"total_us_all_levels": sum(ts), "launches": len(ts)}
