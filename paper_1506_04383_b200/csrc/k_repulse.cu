@@ -699,12 +699,15 @@ __device__ __forceinline__ f2x entropy_r2(f2x X, f2x Y, f2x Z, const float4& sv)
 
 // phi-sum contribution of two pairs with (clamped) r^2 = a, b:
 // q = 0: lg2(a) + lg2(b) = lg2(a b)  (one MUFU);  q > 0: 2^(cq lg2 a) + 2^(cq lg2 b)
-template <bool QPOW>
+// CLAMP = false: q <= kQNoClampE, where r^2 >= kR2Floor bounds cq lg2 r^2 <= 126
+template <bool QPOW, bool CLAMP = true>
 __device__ __forceinline__ float entropy_phi2(float a, float b, float cq) {
     if constexpr (!QPOW) {
         return lg2_approx(a * b);
-    } else {
+    } else if constexpr (CLAMP) {
         return ex2_approx(fminf(cq * lg2_approx(a), kExpClamp)) + ex2_approx(fminf(cq * lg2_approx(b), kExpClamp));
+    } else {
+        return ex2_approx(cq * lg2_approx(a)) + ex2_approx(cq * lg2_approx(b));
     }
 }
 
@@ -712,7 +715,7 @@ __device__ __forceinline__ float entropy_phi2(float a, float b, float cq) {
 #define MM_ENT_POLY 1  // q > 0 energy: the second target pair of every other source uses ex2_poly2 (Q29)
 #endif
 // one source against the thread's 2 x 2 targets (no mask); POLY1: 2^y of group 1 on the FMA pipe
-template <int DIM, bool QPOW, bool POLY1>
+template <int DIM, bool QPOW, bool POLY1, bool CLAMP>
 __device__ __forceinline__ void entropy_src(const float4& sv, const f2x (&X)[2], const f2x (&Y)[2],
                                             const f2x (&Z)[2], float cq, float& acc, int32_t& zt) {
 #pragma unroll
@@ -724,15 +727,15 @@ __device__ __forceinline__ void entropy_src(const float4& sv, const f2x (&X)[2],
         rb = fmaxf(rb, kR2Floor);
         if (QPOW && POLY1 && gg == 1) {
             float ea, eb;
-            upk(ex2_poly2(mul_bc(pk(lg2_approx(ra), lg2_approx(rb)), cq)), ea, eb);
+            upk(ex2_poly2_scaled<CLAMP>(pk(lg2_approx(ra), lg2_approx(rb)), cq, kExpClamp / cq, -125.f / cq), ea, eb);
             acc += ea + eb;
         } else {
-            acc += entropy_phi2<QPOW>(ra, rb, cq);
+            acc += entropy_phi2<QPOW, CLAMP>(ra, rb, cq);
         }
     }
 }
 
-template <int DIM, bool QPOW>
+template <int DIM, bool QPOW, bool CLAMP = true>
 __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* __restrict__ x, float cq,
                                                         TriSched ts, double* __restrict__ partial,
                                                         int32_t* __restrict__ coinc) {
@@ -819,12 +822,12 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
                 if constexpr (QPOW && MM_ENT_POLY) {
 #pragma unroll 2
                     for (; jj + 2 <= cnt; jj += 2) {
-                        entropy_src<DIM, QPOW, false>(sm[jj], X, Y, Z, cq, acc, zt);
-                        entropy_src<DIM, QPOW, true>(sm[jj + 1], X, Y, Z, cq, acc, zt);
+                        entropy_src<DIM, QPOW, false, CLAMP>(sm[jj], X, Y, Z, cq, acc, zt);
+                        entropy_src<DIM, QPOW, true, CLAMP>(sm[jj + 1], X, Y, Z, cq, acc, zt);
                     }
                 }
 #pragma unroll 4
-                for (; jj < cnt; ++jj) entropy_src<DIM, QPOW, false>(sm[jj], X, Y, Z, cq, acc, zt);
+                for (; jj < cnt; ++jj) entropy_src<DIM, QPOW, false, CLAMP>(sm[jj], X, Y, Z, cq, acc, zt);
             } else {
                 for (int jj = 0; jj < cnt; ++jj) {
                     const float4 sv = sm[jj];
@@ -848,7 +851,7 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
                 }
             }
             // coincident pairs entered with r^2 = kR2Floor: remove their contribution
-            if (zt) acc -= (float)zt * entropy_phi2<QPOW>(kR2Floor, 1.f, cq) - (QPOW ? (float)zt : 0.f);
+            if (zt) acc -= (float)zt * entropy_phi2<QPOW, CLAMP>(kR2Floor, 1.f, cq) - (QPOW ? (float)zt : 0.f);
             zc += zt;
             dacc += (double)acc;
         }
@@ -1070,11 +1073,15 @@ cudaError_t launch_entropy_all(int dim, double q, int32_t n, const float* x, con
     LaunchScope ls("entropy_pairs", st);
     const bool qpow = q != 0.0;
     const int G = p.ts.G;
+    // (q/2) |lg2 kR2Floor| <= 126: the q > 0 pair terms cannot overflow, no clamp
+    const bool noclamp = q <= 4.2;
     if (dim == 2) {
-        if (qpow) k_entropy_tri<2, true><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
+        if (qpow && noclamp) k_entropy_tri<2, true, false><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
+        else if (qpow) k_entropy_tri<2, true><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
         else k_entropy_tri<2, false><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
     } else {
-        if (qpow) k_entropy_tri<3, true><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
+        if (qpow && noclamp) k_entropy_tri<3, true, false><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
+        else if (qpow) k_entropy_tri<3, true><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
         else k_entropy_tri<3, false><<<G, kBlock, 0, st>>>(n, x, cq, p.ts, partial, coinc);
     }
     return cudaGetLastError();
