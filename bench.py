@@ -321,8 +321,29 @@ def run_gpu(args):
             def step():
                 return mm.layout(G, S, w.dim, w.alpha, w.q, w.h, [K], w.seed, x_init=x0, out=out)
 
-        for _ in range(args.warmup):
+        # warm-up; for long steps (multilevel configs, seconds each) the per-kernel
+        # launch times are taken during the second warm-up step (library CUDA
+        # events around every launch) instead of in an extra pass after the timed steps
+        prof, prof_steps = None, 0
+        first_ms = 0.0
+        for wi in range(args.warmup):
+            if wi == 1 and first_ms > 1000.0:
+                mm.profile_reset()
+                mm.profile_enable(True)
+                flush.fill_(-1.0)
+                _, rep = step()
+                torch.cuda.synchronize(dev)
+                prof = mm.profile_read()
+                mm.profile_enable(False)
+                prof_steps = 1
+                continue
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
             _, rep = step()
+            e1.record(stream)
+            if wi == 0:
+                torch.cuda.synchronize(dev)
+                first_ms = e0.elapsed_time(e1)
         torch.cuda.synchronize(dev)
 
         # ---- timed region (device-resident inputs)
@@ -346,15 +367,16 @@ def run_gpu(args):
 
         # ---- per-kernel launch times (library CUDA events around every launch) in a
         # separate pass, so that the events' overhead stays out of the timed steps
-        prof_steps = args.steps if ms_step < 200 else 1
-        mm.profile_reset()
-        mm.profile_enable(True)
-        for s in range(prof_steps):
-            flush.fill_(float(s))
-            step()
-        torch.cuda.synchronize(dev)
-        prof = mm.profile_read()
-        mm.profile_enable(False)
+        if prof is None:
+            prof_steps = args.steps if ms_step < 200 else 1
+            mm.profile_reset()
+            mm.profile_enable(True)
+            for s in range(prof_steps):
+                flush.fill_(float(s))
+                step()
+            torch.cuda.synchronize(dev)
+            prof = mm.profile_read()
+            mm.profile_enable(False)
 
         # ---- e2e through the public API with host buffers
         pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
@@ -388,7 +410,7 @@ def run_gpu(args):
         e2e_step()
         torch.cuda.synchronize(dev)
         # long steps (cfg5: seconds each): a few e2e steps bound the run time
-        e2e_steps = args.steps if ms_step < 1000.0 else min(args.steps, 3)
+        e2e_steps = args.steps if ms_step < 1000.0 else min(args.steps, 2)
         ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
         barrier()
         for s in range(e2e_steps):

@@ -46,7 +46,7 @@ def test_single_level_schedule(mm, name, cap):
 
 
 @pytest.mark.parametrize("name,h,n_stop,cap", [("cfg3_mesh32", 0, 100, 25), ("cfg3_mesh64", 2, 200, 25),
-                                               ("cfg5_grid12", 2, 100, 20)])
+                                               ("cfg5_grid12", 2, 100, 20), ("cfg3_mesh256", 2, 1000, 100)])
 def test_multilevel_schedule(mm, name, h, n_stop, cap):
     w = workload(name)
     gs, os_ = _sched(mm, cap)
