@@ -14,7 +14,9 @@ SOURCES = ["k_repulse.cu", "k_gather.cu", "k_hier.cu", "k_fullstress.cu", "k_scl
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",
-         "-I", os.path.join(ROOT, "include")]
+         "-I", os.path.join(ROOT, "include"),
+         # host code: an uninitialised status on an error path is a build error
+         "-Xcompiler", "-Wmaybe-uninitialized", "-Xcompiler", "-Werror=maybe-uninitialized"]
 
 
 def _stale() -> bool:

@@ -79,15 +79,18 @@ def test_dynamic_update(mm):
     assert_energy(rep["energy"], eo[2], "schedule dynamic cfg3_mesh32")
 
 
-@pytest.mark.parametrize("name,dim", [("cfg3_mesh64", 2), ("cfg5_grid12", 3)])
-def test_schedule_sclap_disc(mm, name, dim):
+@pytest.mark.parametrize("name,dim,n_stop,cap", [("cfg3_mesh64", 2, 100, 20), ("cfg5_grid12", 3, 100, 20),
+                                                ("cfg3_mesh256", 2, 1000, 100)])
+def test_schedule_sclap_disc(mm, name, dim, n_stop, cap):
     """The paper's configuration end to end: SCLaP hierarchy (R6), disc
-    prolongation (R7), alpha schedule, h = 2."""
+    prolongation (R7), alpha schedule, h = 2.  mesh256's finest
+    levels run on the tiled path, renumbered (Q30), with SCLaP families of
+    more than two members (the gather's child-list walk)."""
     w = workload(name)
-    gs, os_ = _sched(mm, 20)
+    gs, os_ = _sched(mm, cap)
     x, rep = mm.layout_schedule(mm.graph_to_device(w.graph), mm.sset_to_device(w.S), w.dim, w.q, 2, gs, w.seed,
-                                n_stop=100, sclap=True, disc=True)
-    xo, eo, nl, sw = oracle.layout_schedule(w.graph, w.S, w.dim, w.q, 2, os_, w.seed, n_stop=100, sclap=True, disc=True)
+                                n_stop=n_stop, sclap=True, disc=True)
+    xo, eo, nl, sw = oracle.layout_schedule(w.graph, w.S, w.dim, w.q, 2, os_, w.seed, n_stop=n_stop, sclap=True, disc=True)
     assert rep["levels"] == nl
     eg = oracle.energy(w.S, mm.coords_from_device(x, w.dim), 0.008, w.q)
     assert _rel(rep["energy"], eg[2]) <= 1e-4
