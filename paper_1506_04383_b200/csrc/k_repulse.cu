@@ -822,7 +822,7 @@ __global__ void __launch_bounds__(kBlock) k_entropy_tri(int32_t n, const float* 
                 if constexpr (QPOW && MM_ENT_POLY) {
 #pragma unroll 2
                     for (; jj + 2 <= cnt; jj += 2) {
-                        entropy_src<DIM, QPOW, false, CLAMP>(sm[jj], X, Y, Z, cq, acc, zt);
+                        entropy_src<DIM, QPOW, MM_ENT_POLY >= 2, CLAMP>(sm[jj], X, Y, Z, cq, acc, zt);
                         entropy_src<DIM, QPOW, true, CLAMP>(sm[jj + 1], X, Y, Z, cq, acc, zt);
                     }
                 }
