@@ -90,6 +90,23 @@ def test_argument_errors_before_any_launch(lib):
         mulment.MM_ERR_UNSUPPORTED
     assert lib.mm_build_hierarchy(None, None, 2, 1, 10, 8, 8, ctypes.byref(h), None) == \
         mulment.MM_ERR_INVALID_ARGUMENT
+    # mm_sweeps: NULL S, bad K, aliasing
+    rc = lib.mm_sweeps(None, 2, 0.1, 0.0, None, 0x5000, 0x6000, 3, None, None)
+    assert rc == mulment.MM_ERR_INVALID_ARGUMENT
+    rc = lib.mm_sweeps(ctypes.byref(s), 2, 0.1, 0.0, None, 0x5000, 0x6000, -1, None, None)
+    assert rc == mulment.MM_ERR_INVALID_ARGUMENT
+    rc = lib.mm_sweeps(ctypes.byref(s), 2, 0.1, 0.0, None, 0x5000, 0x5000, 3, None, None)
+    assert rc == mulment.MM_ERR_INVALID_ARGUMENT and b"alias" in lib.mm_last_error()
+    # mm_prolong: bad dim, negative size, NULL parent, aliasing, misaligned float4
+    assert lib.mm_prolong(8, 4, 0x1000, 0x5000, None, 1, 0, 0x6000, None) == mulment.MM_ERR_UNSUPPORTED
+    assert lib.mm_prolong(-1, 2, 0x1000, 0x5000, None, 1, 0, 0x6000, None) == mulment.MM_ERR_INVALID_ARGUMENT
+    assert lib.mm_prolong(8, 2, None, 0x5000, None, 1, 0, 0x6000, None) == mulment.MM_ERR_INVALID_ARGUMENT
+    assert lib.mm_prolong(8, 2, 0x1000, 0x5000, None, 1, 0, 0x5000, None) == mulment.MM_ERR_INVALID_ARGUMENT
+    assert lib.mm_prolong(8, 3, 0x1000, 0x5008, None, 1, 0, 0x6000, None) == mulment.MM_ERR_INVALID_ARGUMENT
+    assert lib.mm_prolong(0, 2, None, None, None, 1, 0, None, None) == mulment.MM_OK  # empty: nothing to do
+    # mm_sweep: a caller workspace that is not 256-B aligned
+    rc = lib.mm_sweep(ctypes.byref(s), 2, 0.1, 0.0, None, 0x5000, 0x6000, None, 0x7010, 1 << 40, None)
+    assert rc == mulment.MM_ERR_INVALID_ARGUMENT and b"256-B" in lib.mm_last_error()
     assert lib.mm_launch_count() == n0  # nothing was launched
 
 
