@@ -324,7 +324,7 @@ def run_gpu(args):
         # warm-up; for long steps (multilevel configs, seconds each) the per-kernel
         # launch times are taken during the second warm-up step (library CUDA
         # events around every launch) instead of in an extra pass after the timed steps
-        prof, prof_steps = None, 0
+        prof, prof_steps, last = None, 0, {}
         first_ms = 0.0
         for wi in range(args.warmup):
             if wi == 1 and first_ms > 1000.0:
@@ -334,6 +334,7 @@ def run_gpu(args):
                 _, rep = step()
                 torch.cuda.synchronize(dev)
                 prof = mm.profile_read()
+                last = {k: mm.profile_last(k, w.sweeps) for k in ("gather_update", "centroid")}
                 mm.profile_enable(False)
                 prof_steps = 1
                 continue
@@ -376,6 +377,7 @@ def run_gpu(args):
                 step()
             torch.cuda.synchronize(dev)
             prof = mm.profile_read()
+            last = {k: mm.profile_last(k, w.sweeps) for k in ("gather_update", "centroid")}
             mm.profile_enable(False)
 
         # ---- e2e through the public API with host buffers
@@ -464,6 +466,27 @@ def run_gpu(args):
             fp32_meas = json.load(f)
     except (OSError, ValueError):
         fp32_meas = None
+    # HBM-bound kernels (a) and (d) at the finest level (its sweeps run last, so
+    # their launches are the last `sweeps` of each kernel), against SURVEY §8(d)'s
+    # algorithmic bytes: gather 4 (n+1) + 12 nnz + 3 b_x n, centroid (b_x + 4) n + b_x k
+    hbm_peak, hbm_src = 6539.2, "fallback: the MEASURED_PEAKS.json value of this pool (6539.2 GB/s)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            hbm_peak, hbm_src = float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs"
+    except (OSError, ValueError, KeyError):
+        pass
+    bx = 8 if w.dim == 2 else 16
+    k0 = rep["k_level"][0] if rep.get("k_level") else 0
+    algo_hbm = {"gather_update": 4 * (n + 1) + 12 * w.S.nnz + 3 * bx * n, "centroid": (bx + 4) * n + bx * k0}
+    roof_hbm = {"peak": hbm_peak, "unit": "GB/s", "peak_source": hbm_src, "level": 0,
+                "bytes_source": "SURVEY §8(d) algorithmic bytes of the finest level per launch"}
+    for kname_h, ts in last.items():
+        if not ts or (kname_h == "centroid" and k0 == 0):
+            continue
+        med = sorted(ts)[len(ts) // 2]
+        gbs = algo_hbm[kname_h] / (med * 1e-3) / 1e9
+        roof_hbm[kname_h] = {"launch_ms_median": med, "launches": len(ts), "bytes_per_launch": algo_hbm[kname_h],
+                             "achieved": gbs, "frac": gbs / hbm_peak}
     step_share = {k: v["total_ms"] / max(prof_steps * dev_ms / args.steps, 1e-9) for k, v in prof.items()}
     gpu_ms = sum(v["total_ms"] for v in prof.values())
     gpu_share = {k: v["total_ms"] / max(gpu_ms, 1e-9) for k, v in prof.items()}
@@ -536,6 +559,7 @@ def run_gpu(args):
                      # q > 0 (lg2 + ex2); kernel (c) moves part of the ex2 to the FMA pipe (Q29)
                      "mufu_per_pair": mufu_pair, "mufu_ceiling_pairs_per_s": mufu_ceiling,
                      "mufu_ceiling_frac": pairs_s_kernel / mufu_ceiling},
+        "roofline_hbm": roof_hbm,
         "levels": rep["n_level"], "k_levels": rep["k_level"],
         # what the timed step computed (last step's report): Eq.(1) of the final layout (coincident
         # non-S pairs, possible in FP32, are left out and counted: DESIGN.md Q6) and the last sweep's

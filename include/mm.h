@@ -324,6 +324,11 @@ MM_API mm_status mm_profile_enable(int on);
 MM_API mm_status mm_profile_reset(void);
 /* writes up to max entries into out (host); *count = number of kernel names */
 MM_API mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count);
+/* the device milliseconds of the LAST (up to max) timed launches of kernel
+ * `name` since mm_profile_reset, in launch order, into ms (host); *count =
+ * how many.  E.g. the finest level of a layout runs last, so its K sweeps'
+ * launches are the last K of each per-sweep kernel.  syncs their events. */
+MM_API mm_status mm_profile_last(const char* name, int32_t max, double* ms, int32_t* count);
 
 #ifdef __cplusplus
 }

@@ -142,6 +142,7 @@ struct PendingEv {
 std::vector<PendingEv> g_pending;
 std::vector<cudaEvent_t> g_event_pool;  // reused timing events (creation is not free)
 std::map<std::string, std::pair<int64_t, double>> g_prof;
+std::vector<std::pair<const char*, float>> g_prof_list;  // every timed launch, in launch order
 
 cudaEvent_t pool_get() {  // caller holds g_prof_mu
     if (!g_event_pool.empty()) {
@@ -656,11 +657,13 @@ mm_status mm_profile_reset(void) {
     }
     g_pending.clear();
     g_prof.clear();
+    g_prof_list.clear();
     return MM_OK;
 }
 
-mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count) {
-    std::lock_guard<std::mutex> g(g_prof_mu);
+namespace {
+// folds the pending launch events into the per-name totals and the ordered list (holds g_prof_mu)
+void prof_fold() {
     for (auto& p : g_pending) {
         cudaError_t e = cudaEventSynchronize(p.b);
         float ms = 0.f;
@@ -668,6 +671,7 @@ mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count) {
             auto& r = g_prof[p.name];
             r.first += 1;
             r.second += ms;
+            g_prof_list.emplace_back(p.name, ms);
         } else {
             cudaGetLastError();
         }
@@ -675,6 +679,24 @@ mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count) {
         g_event_pool.push_back(p.b);
     }
     g_pending.clear();
+}
+}  // namespace
+
+mm_status mm_profile_last(const char* name, int32_t max, double* ms, int32_t* count) {
+    if (!name || (max > 0 && !ms) || !count) { set_err("mm_profile_last: NULL argument"); return MM_ERR_INVALID_ARGUMENT; }
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    prof_fold();
+    int32_t c = 0;
+    for (auto it = g_prof_list.rbegin(); it != g_prof_list.rend() && c < max; ++it)
+        if (strcmp(it->first, name) == 0) ms[c++] = it->second;
+    std::reverse(ms, ms + c);
+    *count = c;
+    return MM_OK;
+}
+
+mm_status mm_profile_read(mm_kernel_profile* out, int32_t max, int32_t* count) {
+    std::lock_guard<std::mutex> g(g_prof_mu);
+    prof_fold();
     int32_t i = 0;
     for (auto& kv : g_prof) {
         if (out && i < max) {

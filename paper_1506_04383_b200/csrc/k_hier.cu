@@ -893,7 +893,8 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
     cudaError_t e = launch_frame(dim, n, x, box, frame, st);
     if (e != cudaSuccess) return e;
     // centroids by representative id (the sort keys); the sweep rewrites them by slot
-    e = launch_centroid(dim, n, k, mptr, mem, x, nullptr, frame, rep_hi, rep_lo, nullptr, tile, st);
+    e = launch_centroid(dim, n, k, mptr, mem, x, nullptr, frame, rep_hi, rep_lo, nullptr, tile, st, nullptr,
+                        "centroid_keys");
     if (e != cudaSuccess) return e;
     {
         LaunchScope ls("order_keys", st);
@@ -919,10 +920,10 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
 
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
                             const int32_t* rord, const float4* frame, float4* rep_hi, float4* rep_lo,
-                            float4* tile_box, int tile, cudaStream_t st, const int2* sbound) {
+                            float4* tile_box, int tile, cudaStream_t st, const int2* sbound, const char* name) {
     if (tile_box != nullptr && k > 0) {
         const cudaError_t e = launch_centroid(dim, n, k, mptr, mem, x, rord, frame, rep_hi, rep_lo, nullptr, tile,
-                                              st, sbound);
+                                              st, sbound, name);
         if (e != cudaSuccess) return e;
         LaunchScope ls("tile_box", st);
         const int nt = (k + tile - 1) / tile;
@@ -930,7 +931,7 @@ cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, 
         else k_tile_box<3><<<nt, tile, 0, st>>>(k, rep_hi, tile_box);
         return cudaGetLastError();
     }
-    LaunchScope ls("centroid", st);
+    LaunchScope ls(name, st);
     // lanes per representative: about 4 members per lane
     const double mean = k > 0 ? (double)n / k : 1.0;
     int G = 1;

@@ -56,7 +56,8 @@ cudaError_t approx_orders(int dim, int32_t n, int32_t k, const int32_t* mptr, co
 // tile_box nullable: else the box of every `tile` slots is written (kernel (c)'s skip test, Q27)
 cudaError_t launch_centroid(int dim, int32_t n, int32_t k, const int32_t* mptr, const int32_t* mem, const float* x,
                             const int32_t* rord, const float4* frame, float4* rep_hi, float4* rep_lo,
-                            float4* tile_box, int tile, cudaStream_t st, const int2* sbound = nullptr);
+                            float4* tile_box, int tile, cudaStream_t st, const int2* sbound = nullptr,
+                            const char* name = "centroid");
 cudaError_t launch_prolong(int dim, int32_t n, const int32_t* parent, const float* xc, uint64_t seed,
                            int32_t level, float* x, cudaStream_t st);
 cudaError_t launch_init_box(int dim, int32_t n, const float* d, int64_t nnz, double* dsum, uint64_t seed,

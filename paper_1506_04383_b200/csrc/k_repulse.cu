@@ -243,6 +243,16 @@ __device__ __forceinline__ void tile_pairs(int cnt, const float4* sm_a, const fl
         }
 #undef MM_SRC
     }
+    if constexpr (G == 1 && DIM == 2 && !QPOW && (BMASK & 1)) {
+        // one packed target pair per thread: batch the reciprocals of every other
+        // SOURCE (instead of every other target group) to keep the FMA / MUFU balance
+#pragma unroll 2
+        for (; jj + 2 <= cnt; jj += 2) {
+            source_pairs<DIM, QPOW, COARSE, G, 1, PAIR_NU, LO, false, CLAMP>(jj, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp);
+            source_pairs<DIM, QPOW, COARSE, G, 0, PAIR_NU, LO, false, CLAMP>(jj + 1, sm_a, sm_b, X, Y, Z, TX, TY, TZ,
+                                                                            cexp);
+        }
+    }
 #pragma unroll UNR
     for (; jj < cnt; ++jj)
         source_pairs<DIM, QPOW, COARSE, G, BMASK, PAIR_NU, LO, false, CLAMP>(jj, sm_a, sm_b, X, Y, Z, TX, TY, TZ, cexp);

@@ -27,7 +27,7 @@ EXPORTS = ["mm_status_string", "mm_last_error", "mm_version", "mm_set_allocator"
            "mm_hierarchy_free", "mm_hierarchy_copy_level", "mm_layout", "mm_layout_schedule", "mm_full_stress",
            "mm_launch_count", "mm_exact_kernel_variant",
            "mm_profile_enable",
-           "mm_profile_reset", "mm_profile_read"]
+           "mm_profile_reset", "mm_profile_read", "mm_profile_last"]
 
 
 class MMError(RuntimeError):
@@ -141,6 +141,7 @@ def load() -> ctypes.CDLL:
     L.mm_profile_enable.argtypes = [ctypes.c_int]; L.mm_profile_enable.restype = ctypes.c_int
     L.mm_profile_reset.argtypes = []; L.mm_profile_reset.restype = ctypes.c_int
     L.mm_profile_read.argtypes = [P(mm_kernel_profile), i32, P(i32)]; L.mm_profile_read.restype = ctypes.c_int
+    L.mm_profile_last.argtypes = [ctypes.c_char_p, i32, P(f64), P(i32)]; L.mm_profile_last.restype = ctypes.c_int
     _lib = L
     return L
 
@@ -446,6 +447,14 @@ def profile_read() -> dict:
     L.mm_profile_read(arr, cnt.value, ctypes.byref(cnt))
     return {arr[i].name.decode(): {"launches": int(arr[i].launches), "total_ms": float(arr[i].total_ms)}
             for i in range(cnt.value)}
+
+
+def profile_last(name: str, count: int) -> list:
+    """Device ms of the last `count` timed launches of kernel `name` (launch order)."""
+    ms = (ctypes.c_double * max(count, 1))()
+    got = ctypes.c_int32()
+    _check(load().mm_profile_last(name.encode(), int(count), ms, ctypes.byref(got)), "mm_profile_last")
+    return [float(ms[i]) for i in range(got.value)]
 
 
 def full_stress(g: DeviceGraph, x):
