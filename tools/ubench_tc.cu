@@ -9,7 +9,7 @@
 #include <cstdlib>
 #include <vector>
 
-#include "../paper_1506_04383_b200/csrc/k_repulse_tc.cuh"
+#include "ubench_tc_accum.cuh"
 
 using namespace mm;
 

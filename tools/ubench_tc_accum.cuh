@@ -1,4 +1,4 @@
-// k_repulse_tc.cuh — kernel (c), far tiles: the pair weights on the FMA / XU pipes,
+// ubench_tc_accum.cuh (builder tool, not part of the library) — kernel (c), far tiles: the pair weights on the FMA / XU pipes,
 // the accumulation over the sources on the 5th-generation tensor cores
 // (tcgen05.mma kind::tf32, A operand = the weights in TMEM, accumulator in TMEM).
 //
@@ -34,7 +34,7 @@
 // Pipelines (mbarriers): bfull / bfree + sfree (smem stage), pfull / wfree (TMEM
 // weight stage, 3 deep), d2full / d2free (accumulator, 2 deep).
 #pragma once
-#include "k_repulse.cuh"
+#include "../paper_1506_04383_b200/csrc/k_repulse.cuh"
 
 namespace mm {
 namespace tc {

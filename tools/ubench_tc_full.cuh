@@ -2,7 +2,7 @@
 // Measured on a B200: 47.6 cycles per 64 pairs per SMSP (production kernel: 33) because TMEM reads (r^2 via
 // tcgen05.ld, the weights as the A operand of the second MMA) run at about 64 B/cycle per SM; without the math
 // 39.5, without the second MMA 36.7, with neither 14.9 (profiles/r02/ubench_tc_full.txt).  The library uses
-// csrc/k_repulse_tc.cuh (r^2 on the FMA pipe, accumulation only on the tensor cores).
+// tools/ubench_tc_accum.cuh (r^2 on the FMA pipe, accumulation only on the tensor cores).
 //
 // kernel (c), far tiles, on the 5th-generation tensor cores
 // (tcgen05.mma kind::tf32, accumulators and the pair weights in TMEM).
