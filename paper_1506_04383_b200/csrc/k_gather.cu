@@ -65,6 +65,9 @@ constexpr int kGatherUnroll = MM_GATHER_UNROLL;
 #ifndef MM_GATHER_SLOAD
 #define MM_GATHER_SLOAD 1  // S rows through the normal (L2-retaining) path; 0: evict-first streaming (measured slower: cfg5 0.105 vs 0.093 ms, cfg3 0.036 vs 0.031 ms; tools/gpu_session89.sh)
 #endif
+#ifndef MM_GATHER_CHUNK
+#define MM_GATHER_CHUNK 0  // > 0: one-lane-per-vertex rows in two-phase chunks of this many entries
+#endif
 #ifndef MM_GATHER_UNROLL_G1
 #define MM_GATHER_UNROLL_G1 2  // one lane per vertex (short rows, e.g. cfg5's 6): unroll 2 measured +10% there (tools/gpu_session87.sh)
 #endif
@@ -202,17 +205,9 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
             const int32_t* __restrict__ colr = a.col + e0;
             const float* __restrict__ dr = a.d + e0;
             const float* __restrict__ wr = a.w + e0;
-            constexpr int kUnr = G == 1 ? MM_GATHER_UNROLL_G1 : kGatherUnroll;
-#pragma unroll kUnr
-            for (int k = lg; k < len; k += G) {
-#if MM_GATHER_SLOAD
-                const int32_t j = __ldg(colr + k);
-                const float dd = __ldg(dr + k), ww = __ldg(wr + k);
-#else
-                const int32_t j = __ldcs(colr + k);
-                const float dd = __ldcs(dr + k), ww = __ldcs(wr + k);
-#endif
-                const float4 xj = load_x<DIM>(a.x, j);
+            // one S entry: the S-pair r-value (removed from the all-pairs / representative
+            // sum) and the attraction term
+            auto s_entry = [&](const float4& xj, float dd, float ww) {
                 const float dx = xi.x - xj.x, dy = xi.y - xj.y;
                 float r2 = fmaf(dx, dx, kEps2);
                 r2 = fmaf(dy, dy, r2);
@@ -221,7 +216,6 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                     dz = xi.z - xj.z;
                     r2 = fmaf(dz, dz, r2);
                 }
-                // S-pair r-value, removed from the all-pairs / representative sum
                 const float inv = inv_pow<QPOW>(r2, cexp);
                 C.x = fmaf(dx, inv, C.x);
                 C.y = fmaf(dy, inv, C.y);
@@ -236,6 +230,43 @@ __global__ void __launch_bounds__(kGBlock, MM_GATHER_MINB) k_gather(GatherArgs a
                 if constexpr (DIM == 3) A.z = fmaf(ww, fmaf(s, dz, xj.z), A.z);
                 const float dev = dist - dd;
                 st = fmaf(ww * dev, dev, st);
+            };
+            if constexpr (G == 1 && MM_GATHER_CHUNK > 0) {
+                // one lane per vertex (short rows): chunks of MM_GATHER_CHUNK entries in two
+                // phases (all index / d / w loads, then all coordinate gathers), so a row of
+                // <= CHUNK entries costs one round trip per level of the col -> x[col] chain.
+                // Slots past the row end are the pair (i, i) with w = d = 0: they add exact
+                // zeros (0 * rcp(eps) = 0), so the sums equal the entry-by-entry loop's bit for bit.
+                constexpr int CH = MM_GATHER_CHUNK;
+                for (int k0 = 0; k0 < len; k0 += CH) {
+                    int32_t jj[CH];
+                    float dd[CH], ww[CH];
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) {
+                        const bool in = k0 + u < len;
+                        jj[u] = in ? __ldg(colr + k0 + u) : (int32_t)i;
+                        dd[u] = in ? __ldg(dr + k0 + u) : 0.f;
+                        ww[u] = in ? __ldg(wr + k0 + u) : 0.f;
+                    }
+                    float4 xj[CH];
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) xj[u] = load_x<DIM>(a.x, jj[u]);
+#pragma unroll
+                    for (int u = 0; u < CH; ++u) s_entry(xj[u], dd[u], ww[u]);
+                }
+            } else {
+                constexpr int kUnr = G == 1 ? MM_GATHER_UNROLL_G1 : kGatherUnroll;
+#pragma unroll kUnr
+                for (int k = lg; k < len; k += G) {
+#if MM_GATHER_SLOAD
+                    const int32_t j = __ldg(colr + k);
+                    const float dd = __ldg(dr + k), ww = __ldg(wr + k);
+#else
+                    const int32_t j = __ldcs(colr + k);
+                    const float dd = __ldcs(dr + k), ww = __ldcs(wr + k);
+#endif
+                    s_entry(load_x<DIM>(a.x, j), dd, ww);
+                }
             }
             if (a.anc != nullptr && lg == 0) {
                 // Eq.(3) excludes the own representative H(i); kernel (c)
