@@ -1,9 +1,9 @@
 """Full-size check of mm_energy (kernel (e)) on the largest config (builder tool).
 
-Step 1 (GPU):  python tools/energy_fullsize_check.py gpu cfg5 OUT.npz
+Step 1 (GPU):  python tests/tools/energy_fullsize_check.py gpu cfg5 OUT.npz
     runs one mm_layout of the config and saves the final layout x (float32) with the energy terms
     mm_layout reported for it.
-Step 2 (CPU):  python tools/energy_fullsize_check.py oracle cfg5 OUT.npz
+Step 2 (CPU):  python tests/tools/energy_fullsize_check.py oracle cfg5 OUT.npz
     evaluates the FP64 oracle's energy (oracle/ only: every unordered pair, about 2.2e12 pow calls at
     cfg5) of that layout and prints both with their relative differences.
 The oracle's own full run of cfg5 is infeasible (~7.5 days single-threaded); this pins
@@ -15,7 +15,7 @@ import time
 
 import numpy as np
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from workloads import configs  # noqa: E402
 
 
