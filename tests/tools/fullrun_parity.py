@@ -3,7 +3,7 @@ against the FP64 oracle's own full run of the same config, on the GPU box's
 host cores (OpenMP over rows).  Prints one JSON line per config:
 E_gpu, E_oracle, their relative difference (bar 1e-3), the oracle energy of
 the GPU layout (kernel error isolated from trajectory divergence) and times.
-Usage: python tools/fullrun_parity.py cfg2 cfg3"""
+Usage: python tests/tools/fullrun_parity.py cfg2 cfg3"""
 import json
 import os
 import sys

@@ -1,6 +1,6 @@
 """One exact sweep, GPU vs FP64 oracle, for the kernel selected by MM_SYM
 (run once per mode): max |x_gpu - x_oracle| / bbox diameter and the RMS error.
-Usage: MM_SYM=2|0 python tools/sym_accuracy.py cfg2_rgg8192 cfg2_rgg16384"""
+Usage: MM_SYM=2|0 python tests/tools/sym_accuracy.py cfg2_rgg8192 cfg2_rgg16384"""
 import os
 import sys
 
