@@ -15,7 +15,7 @@
 // Coordinates are relative to the centre c_b of the target block's box
 // (x' = x - c_b), so |x_i'| <= rho_b and, for an eligible stage,
 // r >= eta max|x_j'|: the cancellation in r2 costs a few ulp(max |x_j'|^2)
-// <= ulp(r2) / eta^2 (Q31).  B2 holds exact two-term TF32 splits
+// <= ulp(r2) / eta^2.  B2 holds exact two-term TF32 splits
 // (hi + lo, 11 significant bits each, round to nearest); the weights are
 // rounded to TF32 (nearest) as they are written to TMEM, so every product is
 // exact and only the FP32 accumulation rounds.  D is drained into FP32
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(256) k_tc_boxes(int32_t n_tgt, const float* __
 
 // eligibility of (block, tile): with c_b the block-box centre, rho_b its half diagonal,
 // D the largest |x_j - c_b| over the tile box and r the box-to-box distance:
-//   r >= eta D  and  r >= eta rho_b   (Q31)
+//   r >= eta D  and  r >= eta rho_b
 __global__ void __launch_bounds__(256) k_tc_elig(int32_t nblk, const float4* __restrict__ blk_box, int32_t ntiles,
                                                  const float4* __restrict__ tile_box, float eta2, int32_t words,
                                                  uint32_t* __restrict__ elig) {

@@ -228,7 +228,7 @@ __global__ void __launch_bounds__(256) k_tc_boxes(int32_t n_tgt, const float* __
 
 // eligibility of (block, tile): with c_b the block-box centre, rho_b its half diagonal,
 // D the largest |x_j - c_b| over the tile box and r the box-to-box distance:
-//   r >= eta D  and  r >= eta rho_b   (Q31)
+//   r >= eta D  and  r >= eta rho_b
 __global__ void __launch_bounds__(256) k_tc_elig(int32_t nblk, const float4* __restrict__ blk_box, int32_t ntiles,
                                                  const float4* __restrict__ tile_box, float eta2, int32_t words,
                                                  uint32_t* __restrict__ elig) {
